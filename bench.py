@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py — kNN_L queries/s on BASELINE.json config 2 (3D, 10M points, k=10).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2] [--scale 1.0]
+
+One step = one kNN_L pass over the config's whole query batch (10M uniform
+queries, seed 3) against the BDL-tree built by one Insert_L of the 10M points
+(seed 2).  `value` = queries/s with queries and outputs resident in HBM (CUDA
+events on the library's stream, L2 flushed between steps); `e2e` = the same
+through the public host API gk_bdl_knn (H2D of the queries and D2H of the
+ids+d2 inside the timed region).  Multi-GPU: N independent replicas (the path
+does not shard into a collective), timed max-over-ranks.
+
+--impl reference times the reference CPU path: the oracle (C++/OpenMP port of
+the paper's algorithms with the reference KnnBuffer/Rng semantics) on all host
+cores, on a bounded sample of the same query batch per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time for cpu_baseline")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_inputs(cfg: int, scale: float):
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(cfg, scale)
+    P = [op[1] for op in script if op[0] == "insert"]
+    K = [op for op in script if op[0] == "knn"]
+    if cfg != 2 and cfg != 1 and cfg != 3:
+        raise SystemExit("bench.py measures the single-insert configs (1, 2, 3); configs 4/5 are parity cases")
+    return d, P[0], K[0][1], K[0][2]
+
+
+def workload_desc(cfg, n, nq, k, d):
+    names = {1: "C1 2D-U-1M BDL-tree, kNN_L self-queries", 2: "C2 3D-U-10M BDL-tree (one Insert_L, seed 2), kNN_L of 10M uniform queries (seed 3)",
+             3: "C3 7D Gaussian-mixture 2M BDL-tree, kNN_L self-queries"}
+    return {"workload": names[cfg], "n_points": n, "n_queries": nq, "k": k, "dim": d, "X": 1024, "leaf": 16,
+            "heuristic": "spatial median", "parallelism": "replicas",
+            "l2": "flushed between timed steps (512 MB write); tree+queries (>500 MB) exceed L2 anyway"}
+
+
+# ------------------------------------------------------------------ CPU ---
+def cpu_knn_rate(P, Q, k, d, target_s: float, sample_cap: int):
+    """Oracle (port of the reference algorithms) kNN_L queries/s on a bounded sample, all host threads."""
+    from oracle import oracle as O
+    if not os.path.exists(O.LIB_PATH):
+        O.build(ref=False)
+    threads = O.max_threads()
+    o = O.BDLTree(d)
+    t0 = time.perf_counter()
+    o.insert(P)
+    build_s = time.perf_counter() - t0
+    probe = min(len(Q), 20000)
+    t0 = time.perf_counter()
+    o.knn(Q[:probe], k)
+    dt = time.perf_counter() - t0
+    m = int(min(len(Q), sample_cap, max(probe, probe * target_s / max(dt, 1e-6))))
+    return o, threads, build_s, m
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    d, P, Q, k = config_inputs(args.config, args.scale)
+    o, threads, build_s, m = cpu_knn_rate(P, Q, k, d, target_s=max(2.0, args.cpu_seconds / max(1, args.steps)),
+                                          sample_cap=len(Q))
+    from oracle import oracle as O  # noqa: F401
+    for _ in range(args.warmup):
+        o.knn(Q[: max(1, m // 10)], k)
+    times = []
+    for s in range(args.steps):
+        lo = (s * m) % max(1, len(Q) - m + 1)
+        t0 = time.perf_counter()
+        o.knn(Q[lo:lo + m], k)
+        times.append(time.perf_counter() - t0)
+    rate = m * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": "kNN_L queries/s", "value": rate, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_desc(args.config, len(P), len(Q), k, d),
+        "cpu_baseline": {"value": rate, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": f"{m} of the {len(Q)} queries per step (kNN_L, k={k}) against the oracle BDL-tree over all "
+                                   f"{len(P)} points (built untimed in {build_s:.1f} s); CPU {cpu_model()}"},
+        "e2e": {"value": rate, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU ---
+def run_gpu(args):
+    import torch
+    import paper_2207_01834_b200 as gk
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    d, P, Q, k = config_inputs(args.config, args.scale)
+    nq = len(Q)
+    g = gk.BDLTree(d, device=dev.index)
+
+    # ---- build (Insert_L / BuildvEB_S), device-resident input
+    P_dev = torch.from_numpy(P).to(dev)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    g.insert_device(P_dev)
+    build_wall = time.perf_counter() - t0
+    build_ms, built = g.last_build_ms()
+    del P_dev
+
+    Q_dev = torch.from_numpy(Q).to(dev)
+    ids_dev = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    d2_dev = torch.empty((nq, k), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.ExternalStream(g.stream(), device=dev)
+
+    # ---- instrumented pass: algorithmic bytes/flops per query (not timed)
+    ctr = g.knn_counted_device(Q_dev, k, ids_dev, d2_dev)
+    bytes_per_q = (ctr["node_bytes"] + ctr["leaf_bytes"]) / nq
+    flops_per_q = ctr["dists"] * (3 * d - 1) / nq
+
+    for _ in range(args.warmup):
+        g.knn_device(Q_dev, k, ids_dev, d2_dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    step_ms, trav_ms = [], []
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.knn_device(Q_dev, k, ids_dev, d2_dev)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            trav_ms.append(g.last_knn_ms()[0])
+    torch.cuda.synchronize(dev)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * nq * args.steps / (total_ms / 1000.0)
+
+    # ---- e2e through the public host API (pinned host buffers, H2D + D2H inside the timed region)
+    Qh = torch.from_numpy(Q).pin_memory().numpy()
+    ids_h = torch.empty((nq, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    d2_h = torch.empty((nq, k), dtype=torch.float64).pin_memory().numpy()
+    g.knn(Qh, k)  # warm
+    e2e_s = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rc = gk.lib().gk_bdl_knn(g._h, Qh.ctypes.data, nq, k, ids_h.ctypes.data, d2_h.ctypes.data)
+        torch.cuda.synchronize(dev)
+        e2e_s.append(time.perf_counter() - t0)
+        assert rc == 0, gk.lib().gk_last_error()
+    e2e_t = sum(e2e_s)
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e = world * nq * len(e2e_s) / e2e_t
+
+    if rank == 0:
+        hbm, peak_src = measured_peaks()
+        k1_ms = statistics.mean(trav_ms)
+        achieved = bytes_per_q * nq / (k1_ms / 1000.0) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+        if os.path.exists(tp):
+            try:
+                tj = json.load(open(tp))
+                if tj.get("config") == args.config:
+                    traffic = tj.get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        cpu = None
+        if not args.no_cpu_baseline:
+            o, threads, build_s, m = cpu_knn_rate(P, Q, k, d, args.cpu_seconds, sample_cap=len(Q))
+            t0 = time.perf_counter()
+            o.knn(Q[:m], k)
+            dt = time.perf_counter() - t0
+            cpu = {"value": m / dt, "unit": "queries/s", "cores": threads, "kind": "port",
+                   "sample": f"first {m} of the {nq} queries (kNN_L, k={k}) against the oracle BDL-tree over all {len(P)} "
+                             f"points (oracle build {build_s:.1f} s, untimed); CPU {cpu_model()}"}
+        line = {
+            "metric": "kNN_L queries/s", "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(args.config, len(P), nq, k, d),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_knn (K1 fused kNN_L traversal)", "k1_ms": k1_ms,
+                         "bytes_per_query": bytes_per_q, "flops_per_query": flops_per_q,
+                         "fp64_gflops": flops_per_q * nq / (k1_ms / 1000.0) / 1e9,
+                         "counters": ctr},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 8,
+                    "d2h_bytes_per_step": nq * k * (4 + 8)},
+            "gpu_launches": 7 * args.steps,
+            "clocks": clk.summary(),
+            "build": {"insert_l_points_per_s": built / (build_ms / 1000.0) if build_ms > 0 else None,
+                      "build_ms": build_ms, "points": built, "wall_s_incl_ingest": build_wall},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,134 @@
+/* gk_bdl.h — C ABI of the B200-native BDL-tree hot path (kNN_L + BuildvEB_S).
+ *
+ * This is the drop-in boundary.  The reference (arxiv 2207.01834 "ParGeo",
+ * /root/reference) declares no batch interface in code; the
+ * entry points below reconstruct the one SPEC.md's `bdltree` module specifies
+ * and the shipped headers' conventions imply:
+ *
+ *   gk_bdl_create   <- BDLTree type, X = 1024, leaf 16
+ *   gk_bdl_insert   <- bdl_build / bdl_insert (Insert_L)     SPEC.md:563-580, PAPER.md:1229-1248 (Alg. 3)
+ *   gk_bdl_erase    <- bdl_erase (Erase_L)                   SPEC.md:581-589, PAPER.md:1255-1269 (Alg. 4)
+ *   gk_bdl_knn      <- bdl_knn (kNN_L) over knn_batch/kNN_S
+ *                      rows = KnnBuffer::extract() order     geokit/kdtree/knn_buffer.hpp:42-46 (sorted by (d2, id))
+ *   point layout    <- Point<D>/PointSet<D>: D doubles, AoS  geokit/core/point.hpp:11-16
+ *   ids             <- PointId = uint32, kNoPoint = ~0u       geokit/core/point.hpp:18-19
+ *   dim range 2..8  <- dispatch_dim (invalid_argument else)  geokit/core/point.hpp:22-35
+ *   errors          <- std::invalid_argument / logic_error   point.hpp:33, seb/orthant.hpp:143
+ *                      mapped to GK_ERR_INVALID / GK_ERR_LOGIC + gk_last_error()
+ *
+ * Conventions: pointers are plain host pointers unless the function name ends
+ * in _device (then they are device pointers on the handle's GPU).  Points are
+ * row-major n x d fp64 (byte-identical to std::vector<Eigen::Matrix<double,D,1>>).
+ * A point's id is its global insertion ordinal (0,1,2,... over all inserts);
+ * points reinserted by Erase_L keep their ids.  kNN output is row-major nq x k,
+ * each row sorted by (squared distance, id), padded with (GK_NO_POINT, +inf)
+ * when fewer than k points are live.  All calls are synchronous with respect
+ * to the host; one handle must be used by one host thread at a time; kNN may
+ * not run concurrently with insert/erase.
+ */
+#ifndef GK_BDL_H
+#define GK_BDL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GK_NO_POINT 0xffffffffu /* geokit::core::kNoPoint */
+
+enum gk_status {
+  GK_OK = 0,
+  GK_ERR_INVALID = 1,     /* std::invalid_argument in the reference */
+  GK_ERR_CUDA = 2,        /* CUDA runtime failure (message in gk_last_error) */
+  GK_ERR_UNSUPPORTED = 3, /* e.g. k > GK_MAX_K */
+  GK_ERR_LOGIC = 4        /* std::logic_error: id space exhausted, bad handle state */
+};
+
+enum gk_heuristic { GK_SPATIAL_MEDIAN = 0, GK_OBJECT_MEDIAN = 1 };
+
+#define GK_MAX_K 32
+#define GK_MAX_LEAF 32
+
+typedef struct gk_bdl gk_bdl; /* opaque handle: owns all device arenas + one CUDA stream */
+
+/* Canonical static-tree node record, exported for parity
+ * checks; identical to the oracle's gko::Node.  168 bytes. */
+typedef struct gk_canon_node {
+  int32_t kind;  /* 0 internal, 1 leaf */
+  int32_t dim;   /* split dimension, -1 for a leaf */
+  int32_t mode;  /* 0 spatial median, 1 object median */
+  int32_t depth;
+  double split;  /* split value (internal) */
+  int32_t left, right;   /* child slots in vEB order, -1 for a leaf */
+  uint32_t start, count; /* the node's point range in the tree's leaf order */
+  double lo[8], hi[8];   /* bounding box (first `dim` entries used) */
+} gk_canon_node;
+
+typedef struct gk_bdl_info {
+  uint64_t F;            /* fullness bitmask (bit i <=> static tree i exists) */
+  uint64_t buffer;       /* points in the buffer tree */
+  uint64_t live;         /* total live points */
+  uint64_t next_id;      /* next insertion ordinal */
+  uint64_t build_size[64];
+  uint64_t live_per_tree[64];
+  uint64_t nodes_per_tree[64];
+  int32_t height_per_tree[64];
+} gk_bdl_info;
+
+typedef struct gk_knn_counters {
+  uint64_t node_bytes;   /* sum over queries of traversal-node bytes the query itself needed */
+  uint64_t leaf_bytes;   /* sum over queries of leaf point bytes (8D + 4 per point) it needed */
+  uint64_t nodes;        /* node visits needed (all queries) */
+  uint64_t leaves;       /* leaf visits needed */
+  uint64_t dists;        /* distance evaluations needed */
+  uint64_t warp_nodes;   /* node loads actually issued (one per warp tile) */
+  uint64_t warp_leaves;  /* leaf loads actually issued (one per warp tile) */
+} gk_knn_counters;
+
+const char* gk_last_error(void);
+const char* gk_version(void);
+
+int gk_bdl_create(int dim, uint32_t buffer_size_X, uint32_t leaf_size, int heuristic, int device, gk_bdl** out);
+int gk_bdl_destroy(gk_bdl* h);
+
+/* Insert_L of n points (host / device row-major n x dim). */
+int gk_bdl_insert(gk_bdl* h, const double* pts, uint64_t n);
+int gk_bdl_insert_device(gk_bdl* h, const double* pts_dev, uint64_t n);
+
+/* Erase_L: tombstone every live point coordinate-equal to some batch point. */
+int gk_bdl_erase(gk_bdl* h, const double* pts, uint64_t n, uint64_t* n_erased);
+int gk_bdl_erase_device(gk_bdl* h, const double* pts_dev, uint64_t n, uint64_t* n_erased);
+
+/* kNN_L: exact k nearest live points of every query, 1 <= k <= GK_MAX_K. */
+int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, double* d2);
+int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev);
+/* Instrumented kNN_L (same results) that also counts the work of §8(d). */
+int gk_bdl_knn_counted_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev,
+                              gk_knn_counters* counters);
+
+int gk_bdl_info_get(gk_bdl* h, gk_bdl_info* info);
+/* Export static tree `tree` (0..63) or the buffer tree (-1): canonical nodes in
+ * vEB slot order, ids and AoS points in leaf order.  Pass NULL to query sizes. */
+int gk_bdl_tree_export(gk_bdl* h, int tree, gk_canon_node* nodes, uint32_t* ids, double* pts,
+                       uint64_t* n_nodes, uint64_t* n_pts);
+/* Stream the handle runs on (cudaStream_t), e.g. to time with events. */
+void* gk_bdl_stream(gk_bdl* h);
+int gk_bdl_sync(gk_bdl* h);
+/* Device time (ms) of the last kNN_L traversal kernel (K1) and of the whole
+ * kNN_L device pipeline, recorded with CUDA events on the handle's stream. */
+int gk_bdl_last_knn_ms(gk_bdl* h, float* traversal_ms, float* total_ms);
+/* Device time (ms) of the last insert's BuildvEB_S work and #points built. */
+int gk_bdl_last_build_ms(gk_bdl* h, float* build_ms, uint64_t* points_built);
+
+/* Seeded input generators (host, OpenMP), restating geokit/generators.hpp:56-63
+ * with side 1 and the BASELINE.json config recipes. */
+int gk_gen_uniform(uint64_t n, int d, uint64_t seed, double* out);
+int gk_gen_mixture(uint64_t n, int d, uint64_t seed, int centres, double sigma, double* out);
+int gk_gen_walk(uint64_t clusters, uint64_t steps, uint64_t seed, double* out);
+int gk_sample_without_replacement(uint64_t n, uint64_t m, uint64_t seed, uint32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GK_BDL_H */

@@ -1,0 +1,256 @@
+"""Python host mirror of the reference's BDL-tree batch interface over the C ABI.
+
+The reference (arxiv 2207.01834, /root/reference) specifies the operations
+bdl_build / bdl_insert / bdl_erase / bdl_knn over
+PointSet<D> inputs (geokit/core/point.hpp:11-19) and reports errors as
+std::invalid_argument / std::logic_error.  This module binds include/gk_bdl.h
+with ctypes and keeps those names, argument meanings and error behaviour:
+invalid arguments raise ValueError, logic errors RuntimeError, CUDA failures
+GpuError.  There is no CPU fallback: if the CUDA library cannot be loaded every
+call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libgkbdl.so")
+
+NO_POINT = 0xFFFFFFFF  # geokit::core::kNoPoint
+MAX_K = 32
+SPATIAL_MEDIAN, OBJECT_MEDIAN = 0, 1
+
+CANON_NODE = np.dtype([
+    ("kind", "<i4"), ("dim", "<i4"), ("mode", "<i4"), ("depth", "<i4"),
+    ("split", "<f8"), ("left", "<i4"), ("right", "<i4"),
+    ("start", "<u4"), ("count", "<u4"),
+    ("lo", "<f8", (8,)), ("hi", "<f8", (8,)),
+])
+
+
+class GpuError(RuntimeError):
+    pass
+
+
+class _Info(C.Structure):
+    _fields_ = [("F", C.c_uint64), ("buffer", C.c_uint64), ("live", C.c_uint64), ("next_id", C.c_uint64),
+                ("build_size", C.c_uint64 * 64), ("live_per_tree", C.c_uint64 * 64),
+                ("nodes_per_tree", C.c_uint64 * 64), ("height_per_tree", C.c_int32 * 64)]
+
+
+class KnnCounters(C.Structure):
+    _fields_ = [("node_bytes", C.c_uint64), ("leaf_bytes", C.c_uint64), ("nodes", C.c_uint64),
+                ("leaves", C.c_uint64), ("dists", C.c_uint64), ("warp_nodes", C.c_uint64),
+                ("warp_leaves", C.c_uint64)]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+_P = C.c_void_p
+_u64 = C.c_uint64
+_lib = None
+
+
+def lib():
+    """Load libgkbdl.so (build it first if it is missing and nvcc is present)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build as _b
+            _b.build()
+        L = C.CDLL(LIB_PATH)
+        L.gk_last_error.restype = C.c_char_p
+        L.gk_version.restype = C.c_char_p
+        L.gk_bdl_create.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(_P)]
+        L.gk_bdl_destroy.argtypes = [_P]
+        L.gk_bdl_insert.argtypes = [_P, _P, _u64]
+        L.gk_bdl_insert_device.argtypes = [_P, _P, _u64]
+        L.gk_bdl_erase.argtypes = [_P, _P, _u64, C.POINTER(_u64)]
+        L.gk_bdl_erase_device.argtypes = [_P, _P, _u64, C.POINTER(_u64)]
+        L.gk_bdl_knn.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
+        L.gk_bdl_knn_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
+        L.gk_bdl_knn_counted_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, C.POINTER(KnnCounters)]
+        L.gk_bdl_info_get.argtypes = [_P, C.POINTER(_Info)]
+        L.gk_bdl_tree_export.argtypes = [_P, C.c_int, _P, _P, _P, C.POINTER(_u64), C.POINTER(_u64)]
+        L.gk_bdl_stream.restype = _P
+        L.gk_bdl_stream.argtypes = [_P]
+        L.gk_bdl_sync.argtypes = [_P]
+        L.gk_bdl_last_knn_ms.argtypes = [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+        L.gk_bdl_last_build_ms.argtypes = [_P, C.POINTER(C.c_float), C.POINTER(_u64)]
+        L.gk_gen_uniform.argtypes = [_u64, C.c_int, _u64, _P]
+        L.gk_gen_mixture.argtypes = [_u64, C.c_int, _u64, C.c_int, C.c_double, _P]
+        L.gk_gen_walk.argtypes = [_u64, _u64, _u64, _P]
+        L.gk_sample_without_replacement.argtypes = [_u64, _u64, _u64, _P]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().gk_last_error().decode(errors="replace")
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise GpuError(msg)
+    if rc == 3:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(_P)
+    return _P(int(a.data_ptr()))  # torch CUDA tensor
+
+
+def _rows(pts, d: int) -> np.ndarray:
+    a = np.ascontiguousarray(pts, dtype=np.float64)
+    if a.ndim == 1 and a.size % d == 0:
+        a = a.reshape(-1, d)
+    if a.ndim != 2 or a.shape[1] != d:
+        raise ValueError(f"expected an (n, {d}) point array, got shape {a.shape}")
+    return a
+
+
+class BDLTree:
+    """Batch-dynamic kd-tree (BDL-tree), device resident on one B200.
+
+    BDLTree(dim, X=1024, leaf_size=16, heuristic=SPATIAL_MEDIAN, device=0)
+      insert(P)        Insert_L  (bdl_insert; bdl_build on an empty tree)
+      erase(P) -> int  Erase_L   (bdl_erase), returns #points tombstoned
+      knn(S, k)        kNN_L     (bdl_knn) -> (ids uint32 (n,k), sqdist float64 (n,k))
+    Device variants take torch CUDA tensors and keep everything in HBM.
+    """
+
+    def __init__(self, dim: int, X: int = 1024, leaf_size: int = 16, heuristic: int = SPATIAL_MEDIAN,
+                 device: int = 0):
+        self.d = int(dim)
+        self.X = int(X)
+        self.leaf_size = int(leaf_size)
+        h = _P()
+        _check(lib().gk_bdl_create(self.d, self.X, self.leaf_size, int(heuristic), int(device), C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().gk_bdl_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # --------------------------------------------------------------- host API
+    def insert(self, pts) -> None:
+        a = _rows(pts, self.d)
+        _check(lib().gk_bdl_insert(self._h, _ptr(a), a.shape[0]))
+
+    build = insert  # bdl_build(P) == bdl_insert(P) on an empty structure
+
+    def erase(self, pts) -> int:
+        a = _rows(pts, self.d)
+        n = _u64(0)
+        _check(lib().gk_bdl_erase(self._h, _ptr(a), a.shape[0], C.byref(n)))
+        return int(n.value)
+
+    def knn(self, queries, k: int):
+        q = _rows(queries, self.d)
+        ids = np.empty((q.shape[0], k), np.uint32)
+        d2 = np.empty((q.shape[0], k), np.float64)
+        _check(lib().gk_bdl_knn(self._h, _ptr(q), q.shape[0], int(k), _ptr(ids), _ptr(d2)))
+        return ids, d2
+
+    # ------------------------------------------------------------- device API
+    def insert_device(self, pts_dev) -> None:
+        _check(lib().gk_bdl_insert_device(self._h, _ptr(pts_dev), int(pts_dev.shape[0])))
+
+    def erase_device(self, pts_dev) -> int:
+        n = _u64(0)
+        _check(lib().gk_bdl_erase_device(self._h, _ptr(pts_dev), int(pts_dev.shape[0]), C.byref(n)))
+        return int(n.value)
+
+    def knn_device(self, q_dev, k: int, ids_dev, d2_dev) -> None:
+        _check(lib().gk_bdl_knn_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), int(k), _ptr(ids_dev),
+                                       _ptr(d2_dev)))
+
+    def knn_counted_device(self, q_dev, k: int, ids_dev, d2_dev) -> dict:
+        c = KnnCounters()
+        _check(lib().gk_bdl_knn_counted_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), int(k), _ptr(ids_dev),
+                                               _ptr(d2_dev), C.byref(c)))
+        return c.as_dict()
+
+    # ------------------------------------------------------------ inspection
+    def info(self) -> dict:
+        i = _Info()
+        _check(lib().gk_bdl_info_get(self._h, C.byref(i)))
+        return dict(F=int(i.F), buffer=int(i.buffer), live=int(i.live), next_id=int(i.next_id),
+                    build_size=np.array(i.build_size[:], np.int64), live_per_tree=np.array(i.live_per_tree[:], np.int64),
+                    nodes_per_tree=np.array(i.nodes_per_tree[:], np.int64),
+                    height_per_tree=np.array(i.height_per_tree[:], np.int32))
+
+    def tree_export(self, tree: int):
+        """(canonical nodes in vEB order, ids, AoS points) of static tree `tree` or the buffer tree (-1)."""
+        nn, npt = _u64(0), _u64(0)
+        _check(lib().gk_bdl_tree_export(self._h, int(tree), None, None, None, C.byref(nn), C.byref(npt)))
+        nodes = np.zeros(nn.value, CANON_NODE)
+        ids = np.zeros(npt.value, np.uint32)
+        pts = np.zeros((npt.value, self.d), np.float64)
+        _check(lib().gk_bdl_tree_export(self._h, int(tree), _ptr(nodes), _ptr(ids), _ptr(pts), C.byref(nn),
+                                        C.byref(npt)))
+        return nodes, ids, pts
+
+    def stream(self) -> int:
+        return int(lib().gk_bdl_stream(self._h) or 0)
+
+    def sync(self) -> None:
+        _check(lib().gk_bdl_sync(self._h))
+
+    def last_knn_ms(self):
+        a, b = C.c_float(), C.c_float()
+        _check(lib().gk_bdl_last_knn_ms(self._h, C.byref(a), C.byref(b)))
+        return float(a.value), float(b.value)
+
+    def last_build_ms(self):
+        a, n = C.c_float(), _u64()
+        _check(lib().gk_bdl_last_build_ms(self._h, C.byref(a), C.byref(n)))
+        return float(a.value), int(n.value)
+
+
+# ---------------------------------------------------------------- inputs ---
+def gen_uniform(n: int, d: int, seed: int) -> np.ndarray:
+    out = np.empty((n, d), np.float64)
+    _check(lib().gk_gen_uniform(n, d, seed, _ptr(out)))
+    return out
+
+
+def gen_mixture(n: int, d: int, seed: int, centres: int = 32, sigma: float = 0.02) -> np.ndarray:
+    out = np.empty((n, d), np.float64)
+    _check(lib().gk_gen_mixture(n, d, seed, centres, sigma, _ptr(out)))
+    return out
+
+
+def gen_walk(clusters: int, steps: int, seed: int) -> np.ndarray:
+    out = np.empty((clusters * steps, 2), np.float64)
+    _check(lib().gk_gen_walk(clusters, steps, seed, _ptr(out)))
+    return out
+
+
+def sample_without_replacement(n: int, m: int, seed: int) -> np.ndarray:
+    out = np.empty(m, np.uint32)
+    _check(lib().gk_sample_without_replacement(n, m, seed, _ptr(out)))
+    return out

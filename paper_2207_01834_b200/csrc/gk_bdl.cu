@@ -1,0 +1,714 @@
+// gk_bdl.cu — the BDL-tree log structure on the device and the C ABI
+// (include/gk_bdl.h).  Host C++ orchestration, device-resident arenas.
+//
+// Reference semantics (restated; the reference ships no code for it):
+//   BDLTree type        SPEC.md:549-555 (buffer tree, statics[i] of X*2^i, bitmask F)
+//   Insert_L (Alg. 3)
+//   Erase_L  (Alg. 4)
+//   Erase_S  (Alg. 2)
+//   kNN_L
+// Frozen decisions (identical in oracle/gk_oracle.cpp):
+//   * ids are global insertion ordinals; Erase_L reinsertions keep their ids
+//   * Insert_L: the LAST |P| mod X points go to the buffer; on overflow the X
+//     oldest buffer points drain; pool = live points of destroyed trees
+//     (ascending tree index, leaf order) ++ drained ++ the first |P| - |P| mod X
+//     points of P; new trees are filled largest-first from contiguous slices
+//     (short/empty with tombstoned sources: an empty one clears its bit)
+//   * Erase: coordinate-exact match, every duplicate; a tombstone is a NaN
+//     written into coordinate 0 (never matches, never enters a k-buffer);
+//     boxes are not tightened; trees with 2*live < build size are gathered
+//     (ascending index, leaf order) and reinserted; buffer excluded from that rule
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gk_common.cuh"
+
+using namespace gk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class T>
+T* dalloc(std::size_t count, cudaStream_t st) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  GK_CUDA(cudaMallocAsync(&p, count * sizeof(T), st));
+  return static_cast<T*>(p);
+}
+template <class T>
+void dfree(T*& p, cudaStream_t st) {
+  if (p) GK_CUDA(cudaFreeAsync(p, st));
+  p = nullptr;
+}
+inline unsigned blocks_for(std::uint64_t n, unsigned t = 256) {
+  return static_cast<unsigned>(std::max<std::uint64_t>(1, (n + t - 1) / t));
+}
+
+// ---------------------------------------------------------------- kernels --
+// AoS rows (n x d) -> SoA [d][stride] + ids = base + i; flags non-finite input
+__global__ void k_ingest(const double* __restrict__ aos, int d, std::uint64_t n, double* __restrict__ soa,
+                         std::uint64_t stride, std::uint32_t* __restrict__ ids, std::uint64_t id_base, int* bad) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < d; ++j) {
+    double x = aos[i * d + j];
+    if (!isfinite(x)) *bad = 1;
+    soa[j * stride + i] = x;
+  }
+  if (ids) ids[i] = static_cast<std::uint32_t>(id_base + i);
+}
+
+// copy SoA rows [0, n) from (src, sstride) to (dst, dstride)
+__global__ void k_copy_soa(const double* __restrict__ src, std::uint64_t sstride, const std::uint32_t* __restrict__ sids,
+                           double* __restrict__ dst, std::uint64_t dstride, std::uint32_t* __restrict__ dids, int d,
+                           std::uint64_t n) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < d; ++j) dst[j * dstride + i] = src[j * sstride + i];
+  dids[i] = sids[i];
+}
+
+__global__ void k_live_flags(const double* __restrict__ c0, std::uint64_t n, std::uint32_t* flags) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) flags[i] = isnan(c0[i]) ? 0u : 1u;
+  else if (i == n) flags[i] = 0u;
+}
+
+__global__ void k_compact(const double* __restrict__ src, std::uint64_t sstride, const std::uint32_t* __restrict__ sids,
+                          const std::uint32_t* __restrict__ flags, const std::uint32_t* __restrict__ pos, int d,
+                          std::uint64_t n, double* __restrict__ dst, std::uint64_t dstride, std::uint32_t* __restrict__ dids) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  const std::uint32_t o = pos[i];
+  for (int j = 0; j < d; ++j) dst[j * dstride + o] = src[j * sstride + i];
+  dids[o] = sids[i];
+}
+
+__global__ void k_gather_ids(std::uint32_t* tree_ids, std::uint32_t* src_idx, const std::uint32_t* __restrict__ arr_ids,
+                             std::uint64_t n) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const std::uint32_t a = tree_ids[i];
+  src_idx[i] = a;
+  tree_ids[i] = arr_ids[a];
+}
+
+__global__ void k_iota(std::uint32_t* out, std::uint64_t n) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = static_cast<std::uint32_t>(i);
+}
+
+// buffer arrival-order live flags from the buffer tree's tombstones
+__global__ void k_buffer_dead(const double* __restrict__ tree_c0, const std::uint32_t* __restrict__ src_idx, std::uint64_t n,
+                              std::uint32_t* flags) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n && isnan(tree_c0[i])) flags[src_idx[i]] = 0u;
+}
+
+// Erase_S for every tree at once: one thread per erase point walks each tree
+// along the children whose (conservative) box contains the point and
+// tombstones coordinate-exact matches with a CAS on coordinate 0 (so every
+// tombstone is counted once even with duplicate batch points).
+template <int D>
+__global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* __restrict__ P, std::uint64_t n,
+                                               unsigned long long* killed) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  double p[D];
+  float pf_lo[D], pf_hi[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    p[j] = P[i * D + j];
+    pf_lo[j] = __double2float_rd(p[j]);
+    pf_hi[j] = __double2float_ru(p[j]);
+  }
+  std::uint64_t stk[kStack];
+  for (int t = 0; t < ts.count; ++t) {
+    const TNode<D>* nodes = static_cast<const TNode<D>*>(ts.t[t].tnodes);
+    double* coords = const_cast<double*>(ts.t[t].coords);
+    const std::uint64_t stride = ts.t[t].stride;
+    int sp = 0;
+    stk[sp++] = ts.t[t].root;
+    unsigned long long local = 0;
+    while (sp > 0) {
+      const std::uint64_t ref = stk[--sp];
+      if (is_leaf_ref(ref)) {
+        const std::uint32_t c = leaf_count(ref);
+        const std::uint64_t s = leaf_start(ref);
+        for (std::uint32_t k = 0; k < c; ++k) {
+          // compare by value (so -0 == +0 as in the oracle), then swap exactly the bits that matched
+          const double c0 = coords[s + k];
+          bool eq = (c0 == p[0]);
+#pragma unroll
+          for (int j = 1; j < D; ++j) eq = eq && (coords[j * stride + s + k] == p[j]);
+          if (eq) {
+            unsigned long long* a = reinterpret_cast<unsigned long long*>(&coords[s + k]);
+            const unsigned long long old = static_cast<unsigned long long>(__double_as_longlong(c0));
+            if (atomicCAS(a, old, 0x7ff8000000000000ULL) == old) ++local;
+          }
+        }
+        continue;
+      }
+      const TNode<D>& nd = nodes[ref];
+#pragma unroll
+      for (int s = 1; s >= 0; --s) {
+        bool in = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) in = in && (pf_hi[j] >= nd.lo[s][j]) && (pf_lo[j] <= nd.hi[s][j]);
+        if (in && sp < kStack) stk[sp++] = nd.ref[s];
+      }
+    }
+    if (local) atomicAdd(&killed[t], local);
+  }
+}
+
+}  // namespace
+
+// ================================================================= handle ==
+struct gk_bdl {
+  int d = 0;
+  std::uint32_t X = 1024, leaf = 16;
+  int heuristic = 0, device = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<DevTree> statics = std::vector<DevTree>(64);
+  std::uint64_t F = 0;
+  double* buf_coords = nullptr;  // arrival order, SoA stride 2X
+  std::uint32_t* buf_ids = nullptr;
+  std::uint64_t buf_n = 0;
+  DevTree buf_tree;
+  std::uint32_t* buf_src = nullptr;  // buffer-tree position -> arrival index
+  std::uint64_t next_id = 0;
+  float knn_ms = 0.f, knn_total_ms = 0.f, build_ms = 0.f;
+  std::uint64_t built_pts = 0;
+  void* cub_tmp = nullptr;
+  std::size_t cub_bytes = 0;
+
+  std::uint64_t bstride() const { return 2ULL * X; }
+
+  void scan(const std::uint32_t* in, std::uint32_t* out, std::uint64_t n) {
+    std::size_t need = 0;
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, static_cast<int>(n), st));
+    if (need > cub_bytes) {
+      if (cub_tmp) GK_CUDA(cudaFreeAsync(cub_tmp, st));
+      cub_bytes = std::max(need, 2 * cub_bytes);
+      GK_CUDA(cudaMallocAsync(&cub_tmp, cub_bytes, st));
+    }
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, need, in, out, static_cast<int>(n), st));
+  }
+
+  // order-preserving copy of the live points of tree T to (dst + off, dstride)
+  std::uint64_t gather_live(const DevTree& T, double* dst, std::uint64_t dstride, std::uint32_t* dids, std::uint64_t off) {
+    if (T.n == 0) return 0;
+    std::uint32_t* flags = dalloc<std::uint32_t>(T.n + 1, st);
+    std::uint32_t* pos = dalloc<std::uint32_t>(T.n + 1, st);
+    k_live_flags<<<blocks_for(T.n + 1), 256, 0, st>>>(T.coords, T.n, flags);
+    scan(flags, pos, T.n + 1);
+    k_compact<<<blocks_for(T.n), 256, 0, st>>>(T.coords, T.n, T.ids, flags, pos, d, T.n, dst + off, dstride, dids + off);
+    GK_CHECK_LAUNCH();
+    dfree(flags, st);
+    dfree(pos, st);
+    return T.live;
+  }
+
+  void rebuild_buffer_tree() {
+    free_tree(buf_tree, st);
+    dfree(buf_src, st);
+    if (buf_n == 0) return;
+    // build over arrival indices, then map them to ids (keeping the map for erase)
+    std::uint32_t* iota = dalloc<std::uint32_t>(buf_n, st);
+    k_iota<<<blocks_for(buf_n), 256, 0, st>>>(iota, buf_n);
+    build_tree(d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), iota, buf_n, buf_tree, st);
+    buf_src = dalloc<std::uint32_t>(buf_n, st);
+    k_gather_ids<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_src, buf_ids, buf_n);
+    GK_CHECK_LAUNCH();
+    dfree(iota, st);
+  }
+
+  // Insert_L of device SoA points (stride sp) with their ids.
+  void insert_l(const double* P, std::uint64_t sp, const std::uint32_t* ids, std::uint64_t n) {
+    if (n == 0) return;
+    const std::uint64_t r = n % X, bulk = n - r;
+    if (r) {
+      k_copy_soa<<<blocks_for(r), 256, 0, st>>>(P + bulk, sp, ids + bulk, buf_coords + buf_n, bstride(), buf_ids + buf_n, d, r);
+      GK_CHECK_LAUNCH();
+      buf_n += r;
+    }
+    const std::uint64_t drained = (buf_n >= X) ? X : 0;
+    const std::uint64_t add = (bulk + drained) / X;
+    if (add == 0) {
+      if (r) rebuild_buffer_tree();
+      return;
+    }
+    const std::uint64_t Fn = F + add;
+    const std::uint64_t destroyed = F & ~Fn, built = Fn & ~F;
+    std::uint64_t pool_n = drained + bulk;
+    for (int i = 0; i < 64; ++i)
+      if (destroyed >> i & 1ULL) pool_n += statics[i].live;
+    double* pool = dalloc<double>(pool_n * d, st);
+    std::uint32_t* pool_ids = dalloc<std::uint32_t>(pool_n, st);
+    std::uint64_t off = 0;
+    for (int i = 0; i < 64; ++i)
+      if (destroyed >> i & 1ULL) {
+        off += gather_live(statics[i], pool, pool_n, pool_ids, off);
+        free_tree(statics[i], st);
+      }
+    if (drained) {
+      k_copy_soa<<<blocks_for(X), 256, 0, st>>>(buf_coords, bstride(), buf_ids, pool + off, pool_n, pool_ids + off, d, X);
+      off += X;
+      // shift the remaining buffer points to the front (arrival order kept)
+      const std::uint64_t rest = buf_n - X;
+      if (rest) {
+        double* tmpc = dalloc<double>(rest * d, st);
+        std::uint32_t* tmpi = dalloc<std::uint32_t>(rest, st);
+        k_copy_soa<<<blocks_for(rest), 256, 0, st>>>(buf_coords + X, bstride(), buf_ids + X, tmpc, rest, tmpi, d, rest);
+        k_copy_soa<<<blocks_for(rest), 256, 0, st>>>(tmpc, rest, tmpi, buf_coords, bstride(), buf_ids, d, rest);
+        dfree(tmpc, st);
+        dfree(tmpi, st);
+      }
+      buf_n = rest;
+    }
+    if (bulk) {
+      k_copy_soa<<<blocks_for(bulk), 256, 0, st>>>(P, sp, ids, pool + off, pool_n, pool_ids + off, d, bulk);
+      off += bulk;
+    }
+    GK_CHECK_LAUNCH();
+    if (r || drained) rebuild_buffer_tree();
+    // build the new trees, largest first, from contiguous pool slices
+    F = Fn;
+    std::uint64_t o = 0;
+    GK_CUDA(cudaEventRecord(ev[2], st));
+    std::uint64_t built_pts_now = 0;
+    for (int i = 63; i >= 0; --i) {
+      if (!(built >> i & 1ULL)) continue;
+      const std::uint64_t cap = static_cast<std::uint64_t>(X) << i;
+      const std::uint64_t c = std::min(cap, pool_n - o);
+      if (c == 0) {
+        F &= ~(1ULL << i);
+        continue;
+      }
+      build_tree(d, static_cast<int>(leaf), heuristic, pool + o, pool_n, pool_ids + o, c, statics[i], st);
+      o += c;
+      built_pts_now += c;
+    }
+    GK_CUDA(cudaEventRecord(ev[3], st));
+    dfree(pool, st);
+    dfree(pool_ids, st);
+    GK_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    GK_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+    build_ms = ms;
+    built_pts = built_pts_now;
+  }
+
+  TreeSet trees(bool include_buffer = true) const {
+    TreeSet ts{};
+    ts.count = 0;
+    for (int i = 63; i >= 0; --i)
+      if ((F >> i & 1ULL) && statics[i].live > 0) {
+        const DevTree& T = statics[i];
+        ts.t[ts.count++] = TreeRef{T.tnodes, T.coords, T.ids, T.n, T.root_ref};
+      }
+    if (include_buffer && buf_n > 0)
+      ts.t[ts.count++] = TreeRef{buf_tree.tnodes, buf_tree.coords, buf_tree.ids, buf_tree.n, buf_tree.root_ref};
+    return ts;
+  }
+
+  std::uint64_t erase_l(const double* P_aos, std::uint64_t n) {
+    if (n == 0) return 0;
+    // all trees (largest first) + buffer tree, one kernel
+    std::vector<int> which;
+    TreeSet ts{};
+    for (int i = 63; i >= 0; --i)
+      if ((F >> i & 1ULL) && statics[i].live > 0) {
+        const DevTree& T = statics[i];
+        ts.t[ts.count++] = TreeRef{T.tnodes, T.coords, T.ids, T.n, T.root_ref};
+        which.push_back(i);
+      }
+    if (buf_n > 0) {
+      ts.t[ts.count++] = TreeRef{buf_tree.tnodes, buf_tree.coords, buf_tree.ids, buf_tree.n, buf_tree.root_ref};
+      which.push_back(-1);
+    }
+    if (ts.count == 0) return 0;
+    unsigned long long* killed = dalloc<unsigned long long>(kMaxTrees, st);
+    GK_CUDA(cudaMemsetAsync(killed, 0, kMaxTrees * 8, st));
+    switch (d) {
+#define GK_D(DD) case DD: k_erase<DD><<<blocks_for(n, 128), 128, 0, st>>>(ts, P_aos, n, killed); break;
+      GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+    }
+    GK_CHECK_LAUNCH();
+    std::vector<unsigned long long> hk(kMaxTrees);
+    GK_CUDA(cudaMemcpyAsync(hk.data(), killed, kMaxTrees * 8, cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaStreamSynchronize(st));
+    dfree(killed, st);
+    std::uint64_t total = 0;
+    for (std::size_t t = 0; t < which.size(); ++t) {
+      total += hk[t];
+      if (which[t] >= 0) statics[which[t]].live -= hk[t];
+      else if (hk[t]) {
+        // drop the dead buffer points, keeping arrival order, and rebuild the buffer tree
+        std::uint32_t* flags = dalloc<std::uint32_t>(buf_n + 1, st);
+        std::uint32_t* pos = dalloc<std::uint32_t>(buf_n + 1, st);
+        std::vector<std::uint32_t> ones(buf_n + 1, 1u);
+        ones[buf_n] = 0;
+        GK_CUDA(cudaMemcpyAsync(flags, ones.data(), (buf_n + 1) * 4, cudaMemcpyHostToDevice, st));
+        k_buffer_dead<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.coords, buf_src, buf_n, flags);
+        scan(flags, pos, buf_n + 1);
+        double* nc = dalloc<double>(bstride() * d, st);
+        std::uint32_t* ni = dalloc<std::uint32_t>(bstride(), st);
+        k_compact<<<blocks_for(buf_n), 256, 0, st>>>(buf_coords, bstride(), buf_ids, flags, pos, d, buf_n, nc, bstride(), ni);
+        GK_CHECK_LAUNCH();
+        dfree(buf_coords, st);
+        dfree(buf_ids, st);
+        buf_coords = nc;
+        buf_ids = ni;
+        buf_n -= hk[t];
+        dfree(flags, st);
+        dfree(pos, st);
+        rebuild_buffer_tree();
+      }
+    }
+    // trees below half of their build size are gathered into R and reinserted
+    std::uint64_t rn = 0;
+    for (int i = 0; i < 64; ++i)
+      if ((F >> i & 1ULL) && 2 * statics[i].live < statics[i].build_size) rn += statics[i].live;
+    std::vector<int> gone;
+    for (int i = 0; i < 64; ++i)
+      if ((F >> i & 1ULL) && 2 * statics[i].live < statics[i].build_size) gone.push_back(i);
+    if (!gone.empty()) {
+      double* R = dalloc<double>(rn * d, st);
+      std::uint32_t* Rid = dalloc<std::uint32_t>(rn, st);
+      std::uint64_t off = 0;
+      for (int i : gone) {
+        off += gather_live(statics[i], R, rn, Rid, off);
+        free_tree(statics[i], st);
+        F &= ~(1ULL << i);
+      }
+      insert_l(R, rn, Rid, rn);
+      dfree(R, st);
+      dfree(Rid, st);
+    }
+    GK_CUDA(cudaStreamSynchronize(st));
+    return total;
+  }
+
+  std::uint64_t live_total() const {
+    std::uint64_t s = buf_n;
+    for (int i = 0; i < 64; ++i)
+      if (F >> i & 1ULL) s += statics[i].live;
+    return s;
+  }
+};
+
+// ==================================================================== C ABI ==
+namespace {
+int fail(int code, const std::string& m) {
+  g_last_error = m;
+  return code;
+}
+template <class Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return GK_OK;
+  } catch (const Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::exception& e) {
+    return fail(GK_ERR_LOGIC, e.what());
+  }
+}
+void need(bool c, const std::string& m) {
+  if (!c) throw Error(GK_ERR_INVALID, m);
+}
+struct DevScope {  // make the handle's GPU current for the call
+  int prev = 0;
+  explicit DevScope(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) GK_CUDA(cudaSetDevice(dev));
+  }
+  ~DevScope() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+const char* gk_last_error(void) { return g_last_error.c_str(); }
+const char* gk_version(void) { return "gk_bdl 0.1 (sm_100a)"; }
+
+int gk_bdl_create(int dim, uint32_t X, uint32_t leaf, int heuristic, int device, gk_bdl** out) {
+  return guard([&] {
+    need(out != nullptr, "out is null");
+    need(dim >= 2 && dim <= 8, "unsupported dimension " + std::to_string(dim));
+    need(X >= 1, "buffer size X must be >= 1");
+    need(leaf >= 1 && leaf <= GK_MAX_LEAF, "leaf size must be in [1, 32]");
+    need(heuristic == GK_SPATIAL_MEDIAN || heuristic == GK_OBJECT_MEDIAN, "unknown splitting heuristic");
+    int ndev = 0;
+    GK_CUDA(cudaGetDeviceCount(&ndev));
+    need(device >= 0 && device < ndev, "no such CUDA device");
+    DevScope ds(device);
+    auto* h = new gk_bdl();
+    h->d = dim;
+    h->X = X;
+    h->leaf = leaf;
+    h->heuristic = heuristic;
+    h->device = device;
+    try {
+      GK_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+      for (auto& e : h->ev) GK_CUDA(cudaEventCreate(&e));
+      cudaMemPool_t pool;
+      GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      std::uint64_t thr = ~0ULL;  // keep freed blocks cached in the pool
+      GK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      h->buf_coords = dalloc<double>(h->bstride() * dim, h->st);
+      h->buf_ids = dalloc<std::uint32_t>(h->bstride(), h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int gk_bdl_destroy(gk_bdl* h) {
+  if (!h) return GK_OK;
+  return guard([&] {
+    DevScope ds(h->device);
+    for (auto& t : h->statics) free_tree(t, h->st);
+    free_tree(h->buf_tree, h->st);
+    dfree(h->buf_src, h->st);
+    dfree(h->buf_coords, h->st);
+    dfree(h->buf_ids, h->st);
+    if (h->cub_tmp) cudaFreeAsync(h->cub_tmp, h->st);
+    cudaStreamSynchronize(h->st);
+    for (auto& e : h->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(h->st);
+    delete h;
+  });
+}
+
+static void insert_device_impl(gk_bdl* h, const double* pts_dev, std::uint64_t n) {
+  if (n == 0) return;
+  if (h->next_id + n > 0xffffffffULL) throw Error(GK_ERR_LOGIC, "id space exhausted (uint32 PointId)");
+  double* soa = dalloc<double>(n * h->d, h->st);
+  std::uint32_t* ids = dalloc<std::uint32_t>(n, h->st);
+  int* bad = dalloc<int>(1, h->st);
+  GK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), h->st));
+  k_ingest<<<blocks_for(n), 256, 0, h->st>>>(pts_dev, h->d, n, soa, n, ids, h->next_id, bad);
+  GK_CHECK_LAUNCH();
+  int hb = 0;
+  GK_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  GK_CUDA(cudaStreamSynchronize(h->st));
+  if (hb) {
+    dfree(soa, h->st);
+    dfree(ids, h->st);
+    dfree(bad, h->st);
+    throw Error(GK_ERR_INVALID, "non-finite coordinate in insert batch");
+  }
+  h->next_id += n;
+  h->insert_l(soa, n, ids, n);
+  dfree(soa, h->st);
+  dfree(ids, h->st);
+  dfree(bad, h->st);
+  GK_CUDA(cudaStreamSynchronize(h->st));
+}
+
+int gk_bdl_insert_device(gk_bdl* h, const double* pts_dev, uint64_t n) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(n == 0 || pts_dev != nullptr, "null points");
+    DevScope ds(h->device);
+    insert_device_impl(h, pts_dev, n);
+  });
+}
+
+int gk_bdl_insert(gk_bdl* h, const double* pts, uint64_t n) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(n == 0 || pts != nullptr, "null points");
+    if (n == 0) return;
+    DevScope ds(h->device);
+    double* d = dalloc<double>(n * h->d, h->st);
+    GK_CUDA(cudaMemcpyAsync(d, pts, n * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    insert_device_impl(h, d, n);
+    dfree(d, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_erase_device(gk_bdl* h, const double* pts_dev, uint64_t n, uint64_t* n_erased) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(n == 0 || pts_dev != nullptr, "null points");
+    DevScope ds(h->device);
+    std::uint64_t k = h->erase_l(pts_dev, n);
+    if (n_erased) *n_erased = k;
+  });
+}
+
+int gk_bdl_erase(gk_bdl* h, const double* pts, uint64_t n, uint64_t* n_erased) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(n == 0 || pts != nullptr, "null points");
+    DevScope ds(h->device);
+    std::uint64_t k = 0;
+    if (n) {
+      double* d = dalloc<double>(n * h->d, h->st);
+      GK_CUDA(cudaMemcpyAsync(d, pts, n * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+      k = h->erase_l(d, n);
+      dfree(d, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+    }
+    if (n_erased) *n_erased = k;
+  });
+}
+
+static void knn_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, int k, std::uint32_t* ids_dev,
+                            double* d2_dev, gk_knn_counters* ctr) {
+  need(k >= 1, "k must be >= 1");
+  if (k > GK_MAX_K) throw Error(GK_ERR_UNSUPPORTED, "k > " + std::to_string(GK_MAX_K) + " is not supported");
+  if (nq == 0) return;
+  TreeSet ts = h->trees();
+  GK_CUDA(cudaEventRecord(h->ev[0], h->st));
+  if (ts.count == 0) {
+    // empty structure: every row is (kNoPoint, +inf)
+    GK_CUDA(cudaMemsetAsync(ids_dev, 0xff, nq * k * sizeof(std::uint32_t), h->st));
+    std::vector<double> inf(nq * k, INFINITY);
+    GK_CUDA(cudaMemcpyAsync(d2_dev, inf.data(), nq * k * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    return;
+  }
+  knn_launch(h->d, k, ts, q_dev, nq, ids_dev, d2_dev, ctr, h->st, h->ev[2], h->ev[3]);
+  GK_CUDA(cudaEventRecord(h->ev[1], h->st));
+  GK_CUDA(cudaStreamSynchronize(h->st));
+  GK_CUDA(cudaEventElapsedTime(&h->knn_ms, h->ev[2], h->ev[3]));
+  GK_CUDA(cudaEventElapsedTime(&h->knn_total_ms, h->ev[0], h->ev[1]));
+}
+
+int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(nq == 0 || (q_dev && ids_dev && d2_dev), "null buffer");
+    DevScope ds(h->device);
+    knn_device_impl(h, q_dev, nq, k, ids_dev, d2_dev, nullptr);
+  });
+}
+
+int gk_bdl_knn_counted_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev,
+                              gk_knn_counters* counters) {
+  return guard([&] {
+    need(h != nullptr && counters != nullptr, "null handle/counters");
+    need(nq == 0 || (q_dev && ids_dev && d2_dev), "null buffer");
+    DevScope ds(h->device);
+    std::memset(counters, 0, sizeof(*counters));
+    knn_device_impl(h, q_dev, nq, k, ids_dev, d2_dev, counters);
+  });
+}
+
+int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, double* d2) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(nq == 0 || (q && ids && d2), "null buffer");
+    need(k >= 1, "k must be >= 1");
+    if (k > GK_MAX_K) throw Error(GK_ERR_UNSUPPORTED, "k > " + std::to_string(GK_MAX_K) + " is not supported");
+    if (nq == 0) return;
+    DevScope ds(h->device);
+    double* dq = dalloc<double>(nq * h->d, h->st);
+    std::uint32_t* di = dalloc<std::uint32_t>(nq * k, h->st);
+    double* dd = dalloc<double>(nq * k, h->st);
+    GK_CUDA(cudaMemcpyAsync(dq, q, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    knn_device_impl(h, dq, nq, k, di, dd, nullptr);
+    GK_CUDA(cudaMemcpyAsync(ids, di, nq * k * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaMemcpyAsync(d2, dd, nq * k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    dfree(dq, h->st);
+    dfree(di, h->st);
+    dfree(dd, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_info_get(gk_bdl* h, gk_bdl_info* info) {
+  return guard([&] {
+    need(h != nullptr && info != nullptr, "null handle/info");
+    std::memset(info, 0, sizeof(*info));
+    info->F = h->F;
+    info->buffer = h->buf_n;
+    info->live = h->live_total();
+    info->next_id = h->next_id;
+    for (int i = 0; i < 64; ++i)
+      if (h->F >> i & 1ULL) {
+        info->build_size[i] = h->statics[i].build_size;
+        info->live_per_tree[i] = h->statics[i].live;
+        info->nodes_per_tree[i] = h->statics[i].n_nodes;
+        info->height_per_tree[i] = h->statics[i].height;
+      }
+  });
+}
+
+int gk_bdl_tree_export(gk_bdl* h, int tree, gk_canon_node* nodes, uint32_t* ids, double* pts, uint64_t* n_nodes,
+                       uint64_t* n_pts) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(tree >= -1 && tree < 64, "tree index out of range");
+    DevScope ds(h->device);
+    const DevTree* T = nullptr;
+    if (tree < 0) T = &h->buf_tree;
+    else {
+      need(h->F >> tree & 1ULL, "static tree " + std::to_string(tree) + " does not exist");
+      T = &h->statics[tree];
+    }
+    if (n_nodes) *n_nodes = T->n_nodes;
+    if (n_pts) *n_pts = T->n;
+    if (nodes && T->n_nodes)
+      GK_CUDA(cudaMemcpyAsync(nodes, T->canon, T->n_nodes * sizeof(gk_canon_node), cudaMemcpyDeviceToHost, h->st));
+    if (ids && T->n) GK_CUDA(cudaMemcpyAsync(ids, T->ids, T->n * 4, cudaMemcpyDeviceToHost, h->st));
+    std::vector<double> soa;
+    if (pts && T->n) {
+      soa.resize(T->n * h->d);
+      GK_CUDA(cudaMemcpyAsync(soa.data(), T->coords, soa.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    }
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    if (pts)
+      for (std::uint64_t i = 0; i < T->n; ++i)
+        for (int j = 0; j < h->d; ++j) pts[i * h->d + j] = soa[j * T->n + i];
+  });
+}
+
+void* gk_bdl_stream(gk_bdl* h) { return h ? static_cast<void*>(h->st) : nullptr; }
+
+int gk_bdl_sync(gk_bdl* h) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_last_knn_ms(gk_bdl* h, float* traversal_ms, float* total_ms) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    if (traversal_ms) *traversal_ms = h->knn_ms;
+    if (total_ms) *total_ms = h->knn_total_ms;
+  });
+}
+
+int gk_bdl_last_build_ms(gk_bdl* h, float* build_ms, uint64_t* points_built) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    if (build_ms) *build_ms = h->build_ms;
+    if (points_built) *points_built = h->built_pts;
+  });
+}
+
+}  // extern "C"

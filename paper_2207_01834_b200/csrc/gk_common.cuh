@@ -1,0 +1,101 @@
+// gk_common.cuh — shared device types of the B200 BDL-tree (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/gk_bdl.h"
+
+namespace gk {
+
+constexpr int kMaxDim = 8;
+constexpr int kDepthCap = 40;     // depth >= 40 -> object-median split (frozen decision)
+constexpr int kStack = 72;        // traversal stack bound: max depth <= 40 + 28 (n < 2^32)
+constexpr int kChunk = 1024;      // points per warp work item in the build passes
+constexpr std::uint64_t kLeafFlag = 1ULL << 63;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GK_CUDA(x)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::gk::Error(GK_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) +      \
+                                          " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+#define GK_CHECK_LAUNCH() GK_CUDA(cudaGetLastError())
+
+// Traversal node (query-optimised mirror of one internal canonical node):
+// both children's boxes, rounded outward to fp32 (conservative, so pruning
+// stays exact), and the two child references.  A child reference is either an
+// internal-node index (rank among internal nodes in vEB order) or, with bit 63
+// set, a leaf: bits [8,56) = first point, bits [0,8) = point count.
+template <int D>
+struct alignas(16) TNode {
+  float lo[2][D];
+  float hi[2][D];
+  std::uint64_t ref[2];
+};
+
+__host__ __device__ inline bool is_leaf_ref(std::uint64_t r) { return (r & kLeafFlag) != 0; }
+__host__ __device__ inline std::uint32_t leaf_count(std::uint64_t r) { return static_cast<std::uint32_t>(r & 0xffu); }
+__host__ __device__ inline std::uint64_t leaf_start(std::uint64_t r) { return (r >> 8) & ((1ULL << 48) - 1); }
+__host__ __device__ inline std::uint64_t make_leaf_ref(std::uint64_t start, std::uint32_t count) {
+  return kLeafFlag | (start << 8) | count;
+}
+
+// order-preserving fp64 <-> uint64 map (for atomicMin/Max on doubles)
+__device__ __forceinline__ std::uint64_t dkey(double x) {
+  std::uint64_t b = static_cast<std::uint64_t>(__double_as_longlong(x));
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double dkey_inv(std::uint64_t k) {
+  std::uint64_t b = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// One static tree on the device.
+struct DevTree {
+  int d = 0;
+  std::uint64_t n = 0;            // points (stride of the SoA arrays)
+  double* coords = nullptr;       // SoA [d][n] in leaf order; tombstone = NaN in coordinate 0
+  std::uint32_t* ids = nullptr;
+  void* tnodes = nullptr;         // TNode<D>[n_internal]
+  std::uint64_t n_internal = 0;
+  std::uint64_t root_ref = 0;
+  gk_canon_node* canon = nullptr; // canonical nodes, vEB slot order
+  std::uint64_t n_nodes = 0;
+  int height = 0;
+  std::uint64_t build_size = 0, live = 0;
+};
+
+// Kernel-side tree descriptor (passed by value in a launch parameter).
+struct TreeRef {
+  const void* tnodes;
+  const double* coords;
+  const std::uint32_t* ids;
+  std::uint64_t stride;
+  std::uint64_t root;
+};
+constexpr int kMaxTrees = 66;
+struct TreeSet {
+  TreeRef t[kMaxTrees];
+  int count;
+};
+
+// build.cu
+void build_tree(int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st);
+void free_tree(DevTree& t, cudaStream_t st);
+
+// knn.cu
+void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq,
+                std::uint32_t* ids_dev, double* d2_dev, gk_knn_counters* counters, cudaStream_t st,
+                cudaEvent_t ev_k0, cudaEvent_t ev_k1);
+
+}  // namespace gk

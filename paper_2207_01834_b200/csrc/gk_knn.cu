@@ -1,0 +1,375 @@
+// gk_knn.cu — kNN_L on the B200 (sm_100a): query reordering (K2) and the fused
+// multi-tree traversal kernel (K1).
+//
+// Reference semantics (restated; no reference code exists for it):
+//   kNN_S  PAPER.md:1206-1224 (descend, sibling fill, bbox include/prune/recurse)
+//   kNN_L  PAPER.md:1285-1287, 1477-1479; SPEC.md:590-597 — one k-buffer per query
+//          reused across the trees, trees visited largest -> smallest, then the buffer tree
+//   KnnBuffer ordering: lexicographic (d2, id), knn_buffer.hpp:18-19, 36-38, 42-46
+// kNN is exact, so the result is a pure function of the live point set: the
+// device traversal only has to (a) compute d2 in the oracle's canonical order
+// (sum_j (q_j - p_j)^2 left to right, no FMA: __dsub_rn/__dmul_rn/__dadd_rn),
+// (b) keep the lexicographic (d2, id) top-k, and (c) prune only when a box's
+// lower-bound distance is STRICTLY greater than the current k-th d2.
+//
+// K1 design: one warp = a tile of 32 Morton-adjacent queries (one per lane)
+// traversing each tree as a packet.  A node is entered when any lane's query
+// still needs it; the warp-uniform reference stack lives in shared memory, the
+// per-lane box lower bounds in a (coalesced, L1-resident) local array.  Node
+// records hold both children's fp32 outward-rounded boxes, so one broadcast
+// 64 B load (3D) decides both children.  A leaf's points are staged once per
+// warp into shared memory with coalesced SoA fp64 loads and every lane scans
+// them against its own query; candidates stay sorted in registers.  All trees
+// of the log structure are walked inside the same kernel, so no per-tree
+// state ever round-trips through HBM.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "gk_common.cuh"
+
+namespace gk {
+namespace {
+
+constexpr int kWarps = 8;  // 256 threads per block
+
+__device__ __forceinline__ bool lexlt(double a, std::uint32_t ia, double b, std::uint32_t ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+template <int K>
+__device__ __forceinline__ void insert_cand(double x, std::uint32_t id, double (&cd)[K], std::uint32_t (&ci)[K]) {
+  if (!lexlt(x, id, cd[K - 1], ci[K - 1])) return;
+#pragma unroll
+  for (int j = K - 1; j > 0; --j) {
+    if (lexlt(x, id, cd[j - 1], ci[j - 1])) {
+      cd[j] = cd[j - 1];
+      ci[j] = ci[j - 1];
+    } else if (lexlt(x, id, cd[j], ci[j])) {
+      cd[j] = x;
+      ci[j] = id;
+    }
+  }
+  if (lexlt(x, id, cd[0], ci[0])) {
+    cd[0] = x;
+    ci[0] = id;
+  }
+}
+
+// lower bound of the canonical d2 of any point inside [lo, hi] (same op order)
+template <int D>
+__device__ __forceinline__ double box_mindist(const double (&q)[D], const float* lo, const float* hi) {
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double l = static_cast<double>(lo[j]), h = static_cast<double>(hi[j]);
+    double t = 0.0;
+    if (q[j] < l) t = __dsub_rn(l, q[j]);
+    else if (q[j] > h) t = __dsub_rn(q[j], h);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return s;
+}
+
+template <int D, int K>
+__global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const double* __restrict__ Q,
+                                                     const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
+                                                     std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
+                                                     unsigned long long* __restrict__ counters) {
+  __shared__ std::uint64_t s_stack[kWarps][kStack];
+  __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
+  __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
+
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const std::uint64_t qi = (static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+  const bool active = qi < nq;
+  std::uint32_t orig = 0;
+  double q[D];
+  if (active) {
+    orig = perm ? perm[qi] : static_cast<std::uint32_t>(qi);
+#pragma unroll
+    for (int j = 0; j < D; ++j) q[j] = Q[static_cast<std::uint64_t>(orig) * D + j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < D; ++j) q[j] = 0.0;
+  }
+  double cd[K];
+  std::uint32_t ci[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    cd[j] = __longlong_as_double(0x7ff0000000000000LL);  // +inf, kNoPoint: KnnBuffer's initial bound
+    ci[j] = GK_NO_POINT;
+  }
+  float mdst[kStack];
+  const bool count = counters != nullptr;
+  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0;
+
+  for (int t = 0; t < ts.count; ++t) {
+    const TNode<D>* __restrict__ nodes = static_cast<const TNode<D>*>(ts.t[t].tnodes);
+    const double* __restrict__ coords = ts.t[t].coords;
+    const std::uint32_t* __restrict__ ids = ts.t[t].ids;
+    const std::uint64_t stride = ts.t[t].stride;
+    std::uint64_t ref = ts.t[t].root;
+    bool need = active;
+    int sp = 0;
+    while (true) {
+      if (is_leaf_ref(ref)) {
+        const std::uint32_t c = leaf_count(ref);
+        const std::uint64_t s = leaf_start(ref);
+        __syncwarp();
+        if (lane < static_cast<int>(c)) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) s_pts[w][j * GK_MAX_LEAF + lane] = coords[j * stride + s + lane];
+          s_ids[w][lane] = ids[s + lane];
+        }
+        __syncwarp();
+        if (active) {
+          for (std::uint32_t p = 0; p < c; ++p) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              const double tt = __dsub_rn(q[j], s_pts[w][j * GK_MAX_LEAF + p]);
+              d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
+            }
+            insert_cand<K>(d2, s_ids[w][p], cd, ci);
+          }
+        }
+        if (count) {
+          if (need) { c_leaves++; c_dists += c; }
+          c_wl++;
+        }
+      } else {
+        const TNode<D>& nd = nodes[ref];
+        float lo0[D], hi0[D], lo1[D], hi1[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          lo0[j] = nd.lo[0][j]; hi0[j] = nd.hi[0][j];
+          lo1[j] = nd.lo[1][j]; hi1[j] = nd.hi[1][j];
+        }
+        const std::uint64_t r0 = nd.ref[0], r1 = nd.ref[1];
+        if (count) {
+          if (need) c_nodes++;
+          c_wn++;
+        }
+        const double m0 = box_mindist<D>(q, lo0, hi0);
+        const double m1 = box_mindist<D>(q, lo1, hi1);
+        const double kth = cd[K - 1];
+        const bool w0 = active && m0 <= kth, w1 = active && m1 <= kth;
+        const unsigned b0 = __ballot_sync(0xffffffffu, w0), b1 = __ballot_sync(0xffffffffu, w1);
+        if (b0 && b1) {
+          // near child first, by majority of the lanes that want both (else by lane count)
+          const unsigned both = b0 & b1;
+          int first;
+          if (both) {
+            const unsigned pref0 = __ballot_sync(0xffffffffu, w0 && w1 && m0 <= m1);
+            first = (2 * __popc(pref0) >= __popc(both)) ? 0 : 1;
+          } else {
+            first = (__popc(b0) >= __popc(b1)) ? 0 : 1;
+          }
+          const std::uint64_t rs = first ? r0 : r1;
+          const double ms = first ? m0 : m1;
+          if (lane == 0) s_stack[w][sp] = rs;
+          mdst[sp] = active ? __double2float_rd(ms) : __int_as_float(0x7f800000);
+          ++sp;
+          ref = first ? r1 : r0;
+          need = first ? w1 : w0;
+          continue;
+        } else if (b0) {
+          ref = r0; need = w0;
+          continue;
+        } else if (b1) {
+          ref = r1; need = w1;
+          continue;
+        }
+      }
+      // pop the next subtree some lane still needs
+      bool found = false;
+      __syncwarp();
+      while (sp > 0) {
+        --sp;
+        const bool nl = active && static_cast<double>(mdst[sp]) <= cd[K - 1];
+        if (__any_sync(0xffffffffu, nl)) {
+          ref = s_stack[w][sp];
+          need = nl;
+          found = true;
+          break;
+        }
+      }
+      if (!found) break;
+    }
+  }
+
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < k) {
+        out_ids[static_cast<std::uint64_t>(orig) * k + j] = ci[j];
+        out_d2[static_cast<std::uint64_t>(orig) * k + j] = cd[j];
+      }
+  }
+  if (count) {
+    const unsigned long long node_b = sizeof(TNode<D>), pt_b = 8 * D + 4;
+    unsigned long long v[5] = {c_nodes, c_leaves, c_dists, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    if (lane == 0) {
+      atomicAdd(&counters[0], v[0] * node_b);
+      atomicAdd(&counters[1], v[2] * pt_b);
+      atomicAdd(&counters[2], v[0]);
+      atomicAdd(&counters[3], v[1]);
+      atomicAdd(&counters[4], v[2]);
+      atomicAdd(&counters[5], c_wn);
+      atomicAdd(&counters[6], c_wl);
+    }
+  }
+}
+
+// --------------------------------------------------------------- K2: order --
+template <int D>
+__global__ void k_qbox(const double* __restrict__ Q, std::uint64_t nq, unsigned long long* box) {
+  double lo[D], hi[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) { lo[j] = __longlong_as_double(0x7ff0000000000000LL); hi[j] = -lo[j]; }
+  for (std::uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double x = Q[i * D + j];
+      lo[j] = fmin(lo[j], x);
+      hi[j] = fmax(hi[j], x);
+    }
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[j] = fmin(lo[j], __shfl_xor_sync(0xffffffffu, lo[j], o));
+      hi[j] = fmax(hi[j], __shfl_xor_sync(0xffffffffu, hi[j], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      atomicMin(&box[2 * j], dkey(lo[j]));
+      atomicMax(&box[2 * j + 1], dkey(hi[j]));
+    }
+}
+
+template <int D>
+__global__ void k_morton(const double* __restrict__ Q, std::uint64_t nq, const unsigned long long* __restrict__ box,
+                         std::uint32_t* keys, std::uint32_t* idx) {
+  constexpr int B = 32 / D;
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nq) return;
+  std::uint32_t cell[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double lo = dkey_inv(box[2 * j]), hi = dkey_inv(box[2 * j + 1]);
+    const double ext = hi - lo;
+    double f = ext > 0.0 ? (Q[i * D + j] - lo) / ext : 0.0;
+    int c = static_cast<int>(f * static_cast<double>(1u << B));
+    c = c < 0 ? 0 : (c > static_cast<int>((1u << B) - 1) ? static_cast<int>((1u << B) - 1) : c);
+    cell[j] = static_cast<std::uint32_t>(c);
+  }
+  std::uint32_t key = 0;
+#pragma unroll
+  for (int b = B - 1; b >= 0; --b)
+#pragma unroll
+    for (int j = 0; j < D; ++j) key = (key << 1) | ((cell[j] >> b) & 1u);
+  keys[i] = key;
+  idx[i] = static_cast<std::uint32_t>(i);
+}
+
+template <int D, int K>
+void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, int k, std::uint32_t* ids,
+              double* d2, unsigned long long* ctr, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
+  k_knn<D, K><<<blocks, kWarps * 32, 0, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
+}
+
+template <int D>
+void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, std::uint32_t* ids,
+              double* d2, unsigned long long* ctr, cudaStream_t st) {
+  if (k <= 1) launch_k<D, 1>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 2) launch_k<D, 2>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 4) launch_k<D, 4>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 5) launch_k<D, 5>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 8) launch_k<D, 8>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 10) launch_k<D, 10>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 16) launch_k<D, 16>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+}
+
+template <int D>
+void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, cudaStream_t st) {
+  unsigned long long* box = nullptr;
+  std::uint32_t *keys = nullptr, *keys2 = nullptr, *idx = nullptr;
+  GK_CUDA(cudaMallocAsync(&box, 2 * D * sizeof(unsigned long long), st));
+  GK_CUDA(cudaMallocAsync(&keys, nq * 4, st));
+  GK_CUDA(cudaMallocAsync(&keys2, nq * 4, st));
+  GK_CUDA(cudaMallocAsync(&idx, nq * 4, st));
+  std::vector<unsigned long long> init(2 * D);
+  for (int j = 0; j < D; ++j) { init[2 * j] = ~0ULL; init[2 * j + 1] = 0ULL; }
+  GK_CUDA(cudaMemcpyAsync(box, init.data(), init.size() * 8, cudaMemcpyHostToDevice, st));
+  const unsigned gb = static_cast<unsigned>(std::min<std::uint64_t>((nq + 255) / 256, 148 * 8));
+  k_qbox<D><<<gb, 256, 0, st>>>(Q, nq, box);
+  k_morton<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, box, keys, idx);
+  GK_CHECK_LAUNCH();
+  void* tmp = nullptr;
+  std::size_t tb = 0;
+  const int bits = (32 / D) * D;
+  GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, perm_out, static_cast<int>(nq), 0, bits, st));
+  GK_CUDA(cudaMallocAsync(&tmp, tb, st));
+  GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, perm_out, static_cast<int>(nq), 0, bits, st));
+  GK_CUDA(cudaFreeAsync(tmp, st));
+  GK_CUDA(cudaFreeAsync(box, st));
+  GK_CUDA(cudaFreeAsync(keys, st));
+  GK_CUDA(cudaFreeAsync(keys2, st));
+  GK_CUDA(cudaFreeAsync(idx, st));
+}
+
+}  // namespace
+
+void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq, std::uint32_t* ids_dev,
+                double* d2_dev, gk_knn_counters* counters, cudaStream_t st, cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+  if (nq == 0) return;
+  if (nq >= 0xffffffffULL) throw Error(GK_ERR_INVALID, "kNN batch larger than 2^32-1 queries");
+  std::uint32_t* perm = nullptr;
+  GK_CUDA(cudaMallocAsync(&perm, nq * 4, st));
+  unsigned long long* ctr = nullptr;
+  if (counters) {
+    GK_CUDA(cudaMallocAsync(&ctr, 8 * sizeof(unsigned long long), st));
+    GK_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st));
+  }
+  switch (d) {
+#define GK_D(DD)                                                   \
+  case DD:                                                         \
+    order_queries<DD>(q_dev, nq, perm, st);                        \
+    if (ev_k0) GK_CUDA(cudaEventRecord(ev_k0, st));                \
+    launch_d<DD>(k, trees, q_dev, perm, nq, ids_dev, d2_dev, ctr, st); \
+    if (ev_k1) GK_CUDA(cudaEventRecord(ev_k1, st));                \
+    break;
+    GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+  GK_CHECK_LAUNCH();
+  if (counters) {
+    unsigned long long h[8];
+    GK_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaStreamSynchronize(st));
+    counters->node_bytes = h[0];
+    counters->leaf_bytes = h[1];
+    counters->nodes = h[2];
+    counters->leaves = h[3];
+    counters->dists = h[4];
+    counters->warp_nodes = h[5];
+    counters->warp_leaves = h[6];
+    GK_CUDA(cudaFreeAsync(ctr, st));
+  }
+  GK_CUDA(cudaFreeAsync(perm, st));
+}
+
+}  // namespace gk

@@ -1,0 +1,43 @@
+"""The C-ABI library loads and exports every symbol include/gk_bdl.h declares
+(no compute call: this runs without a GPU)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "gk_bdl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gk_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(gk):
+    names = declared_symbols()
+    assert len(names) >= 20
+    L = gk.lib()
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+
+
+def test_canon_node_layout_matches_oracle(oracle, gk):
+    from paper_2207_01834_b200.bdltree import CANON_NODE
+    assert CANON_NODE.itemsize == 168 == oracle.CANON_NODE.itemsize == oracle.lib().gko_node_size()
+
+
+def test_version_and_invalid_args(gk):
+    L = gk.lib()
+    assert b"sm_100a" in L.gk_version()
+    import pytest
+    with pytest.raises(ValueError):
+        gk.BDLTree(9)  # dispatch_dim: 2..8 only (point.hpp:22-35)
+    with pytest.raises(ValueError):
+        gk.BDLTree(3, leaf_size=0)
+
+
+def test_library_is_sm100a():
+    lib = os.path.join(ROOT, "paper_2207_01834_b200", "_lib", "libgkbdl.so")
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact: neighbour ids, the built trees' point permutation, canonical node
+records (vEB slots, splits, boxes), the log structure's F / buffer / live
+counts.  Squared distances: within 1e-12 relative (north star); they come out
+bit-identical because both sides use the same no-FMA operation order.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+FIELDS = ("kind", "dim", "mode", "depth", "split", "left", "right", "start", "count", "lo", "hi")
+
+
+def assert_knn_equal(a, b, what=""):
+    ia, da = a
+    ib, db = b
+    assert ia.shape == ib.shape, what
+    bad = np.nonzero((ia != ib).any(1))[0]
+    assert len(bad) == 0, f"{what}: {len(bad)} rows differ, first {bad[:5]}: {ia[bad[:1]]} vs {ib[bad[:1]]}"
+    fin = np.isfinite(db)
+    assert np.array_equal(np.isfinite(da), fin), what
+    rel = np.abs(da[fin] - db[fin]) / np.maximum(np.abs(db[fin]), 1e-300)
+    assert (rel <= RTOL).all(), f"{what}: max rel {rel.max()}"
+
+
+def assert_tree_equal(g, o, i):
+    gn, gi, gp = g.tree_export(i)
+    on, oi, op = o.tree_export(i)
+    assert np.array_equal(gi, oi), f"tree {i}: permutation differs"
+    np.testing.assert_array_equal(gp, op)
+    assert len(gn) == len(on), f"tree {i}: {len(gn)} vs {len(on)} nodes"
+    for f in FIELDS:
+        assert np.array_equal(gn[f], on[f]), f"tree {i}: node field {f} differs"
+
+
+def assert_struct_equal(g, o, trees=True):
+    gi, oi = g.info(), o.stats()
+    assert gi["F"] == oi["F"] and gi["buffer"] == oi["buffer"]
+    assert np.array_equal(gi["build_size"], oi["build_size"])
+    assert np.array_equal(gi["live_per_tree"], oi["live"])
+    if trees:
+        for i in range(64):
+            if gi["F"] >> i & 1:
+                assert_tree_equal(g, o, i)
+
+
+def run_script(gk, oracle, d, script, X=1024, leaf=16, heur=0, trees=True):
+    g = gk.BDLTree(d, X=X, leaf_size=leaf, heuristic=heur)
+    o = oracle.BDLTree(d, X=X, leaf=leaf, heuristic=heur)
+    for step, op in enumerate(script):
+        if op[0] == "insert":
+            g.insert(op[1]); o.insert(op[1])
+            assert_struct_equal(g, o, trees)
+        elif op[0] == "erase":
+            kg, ko = g.erase(op[1]), o.erase(op[1])
+            assert kg == ko, f"step {step}: erased {kg} vs {ko}"
+            assert_struct_equal(g, o, trees)
+        else:
+            assert_knn_equal(g.knn(op[1], op[2]), o.knn(op[1], op[2]), f"step {step} knn k={op[2]}")
+    return g, o
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_baseline_configs_reduced(gk, oracle, cfg):
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(cfg, scale=0.01)
+    run_script(gk, oracle, d, script)
+
+
+def test_golden_fixture(gk):
+    import os
+    g0 = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_small.npz"))
+    g = gk.BDLTree(3)
+    g.insert(g0["P"])
+    ids, d2 = g.knn(g0["Q"], 10)
+    assert np.array_equal(ids, g0["ids"]) and np.array_equal(d2, g0["d2"])
+    nodes, tids, tpts = g.tree_export(1)
+    assert nodes.view(np.uint8).tobytes() == g0["tree1_nodes"].tobytes()
+    assert np.array_equal(tids, g0["tree1_ids"]) and np.array_equal(tpts, g0["tree1_pts"])
+
+
+def test_golden_veb_layout(gk, oracle):  # SPEC.md:476 / Fig. vebconstruct, through BuildvEB_S on the GPU
+    P = np.array([(0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (3, 0), (2, 1), (3, 1)], float)
+    g = gk.BDLTree(2, X=8, leaf_size=1)
+    g.insert(P)
+    nodes, _, _ = g.tree_export(0)
+    assert [nodes[1]["left"], nodes[1]["right"], nodes[2]["left"], nodes[2]["right"]] == [3, 6, 9, 12]
+    on, _, _ = oracle.Tree(P, leaf=1).export()
+    assert nodes.tobytes() == on.tobytes()
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("k", [1, 3, 10, 16, 32])
+def test_dims_and_k(gk, oracle, d, k):
+    rng = np.random.default_rng(100 * d + k)
+    P = rng.random((6000, d))
+    Q = rng.random((700, d))
+    run_script(gk, oracle, d, [("insert", P), ("knn", Q, k), ("knn", P[:500], k)], X=256)
+
+
+@pytest.mark.parametrize("leaf", [1, 2, 8, 32])
+@pytest.mark.parametrize("heur", [0, 1])
+def test_leaf_and_heuristic(gk, oracle, leaf, heur):
+    rng = np.random.default_rng(leaf + 10 * heur)
+    P = rng.random((5000, 3))
+    run_script(gk, oracle, 3, [("insert", P), ("knn", rng.random((500, 3)), 7)], X=512, leaf=leaf, heur=heur)
+
+
+def test_degenerate_duplicates(gk, oracle):
+    """heavy duplicates: degenerate spatial splits fall back to the (x_c, id) object median"""
+    rng = np.random.default_rng(5)
+    P = np.round(rng.random((20000, 2)) * 4) / 4
+    P[:3000] = 0.5  # one point repeated 3000 times
+    P[3000:3100, 0] = -0.0
+    P[3100:3200, 0] = 0.0
+    Q = np.concatenate([rng.random((300, 2)), P[:50]])
+    g, o = run_script(gk, oracle, 2, [("insert", P), ("knn", Q, 16), ("erase", P[2990:3005]), ("knn", Q, 5)], X=1000)
+
+
+def test_deep_spatial_tree(gk, oracle):
+    """exponentially spaced coordinates drive spatial splits past the depth cap (object median below it)"""
+    x = 2.0 ** -np.arange(1, 300, dtype=np.float64)
+    P = np.stack([x, np.zeros_like(x)], 1)
+    P = np.concatenate([P, np.random.default_rng(1).random((500, 2))])
+    run_script(gk, oracle, 2, [("insert", P), ("knn", P, 4)], X=len(P), leaf=2)
+
+
+def test_empty_and_short(gk, oracle):
+    g = gk.BDLTree(3)
+    ids, d2 = g.knn(np.zeros((4, 3)), 5)  # empty structure: padded rows
+    assert (ids == gk.NO_POINT).all() and np.isinf(d2).all()
+    P = np.random.default_rng(2).random((3, 3))
+    run_script(gk, oracle, 3, [("insert", P), ("knn", np.random.default_rng(3).random((10, 3)), 8)])
+
+
+def test_errors(gk):
+    g = gk.BDLTree(3)
+    with pytest.raises(NotImplementedError):
+        g.knn(np.zeros((1, 3)), 33)
+    with pytest.raises(ValueError):
+        g.knn(np.zeros((1, 3)), 0)
+    with pytest.raises(ValueError):
+        g.insert(np.array([[0.0, np.nan, 1.0]]))
+    with pytest.raises(ValueError):
+        g.insert(np.zeros((2, 4)))
+    assert g.info()["live"] == 0
+
+
+def test_insert_figure_X4(gk, oracle):  # SPEC.md:578-580 with X = 4
+    rng = np.random.default_rng(4)
+    script = [("insert", rng.random((4, 2))), ("insert", rng.random((5, 2))), ("insert", rng.random((5, 2))),
+              ("insert", rng.random((3, 2))), ("knn", rng.random((50, 2)), 3)]
+    g, o = run_script(gk, oracle, 2, script, X=4)
+    assert g.info()["F"] == 4 and g.info()["buffer"] == 1
+
+
+def test_erase_all_and_absent(gk, oracle):
+    rng = np.random.default_rng(6)
+    P = rng.random((3000, 2))
+    script = [("insert", P), ("erase", rng.random((100, 2))), ("knn", P[:20], 3), ("erase", P),
+              ("knn", P[:20], 3), ("insert", P[:1500]), ("knn", P[:40], 4)]
+    g, o = run_script(gk, oracle, 2, script, X=128)
+    assert g.info()["live"] == 1500
+
+
+def test_model_scripts(gk, oracle):
+    """random insert/erase/kNN scripts with a small coordinate universe (duplicates, absent erases,
+    half-capacity rebuilds, tombstoned-pool re-decomposition)"""
+    rng = np.random.default_rng(77)
+    for s in range(12):
+        d = int(rng.integers(2, 5))
+        X = int(rng.choice([4, 16, 64]))
+        script = []
+        for op in range(int(rng.integers(5, 15))):
+            r = rng.random()
+            if r < 0.5:
+                script.append(("insert", np.round(rng.random((int(rng.integers(0, 4 * X)), d)) * 6) / 6))
+            elif r < 0.8:
+                script.append(("erase", np.round(rng.random((int(rng.integers(0, 2 * X)), d)) * 6) / 6))
+            else:
+                script.append(("knn", rng.random((64, d)), int(rng.integers(1, 9))))
+        run_script(gk, oracle, d, script, X=X)
+
+
+def test_device_api_matches_host_api(gk):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(9)
+    P = rng.random((50000, 3))
+    Q = rng.random((20000, 3))
+    a = gk.BDLTree(3)
+    a.insert(P)
+    b = gk.BDLTree(3)
+    b.insert_device(torch.from_numpy(P).cuda())
+    ids = torch.empty((len(Q), 10), dtype=torch.int32, device="cuda")
+    d2 = torch.empty((len(Q), 10), dtype=torch.float64, device="cuda")
+    b.knn_device(torch.from_numpy(Q).cuda(), 10, ids, d2)
+    torch.cuda.synchronize()
+    ra = a.knn(Q, 10)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), ra[0]) and np.array_equal(d2.cpu().numpy(), ra[1])
+    c = b.knn_counted_device(torch.from_numpy(Q).cuda(), 10, ids, d2)
+    assert c["nodes"] > 0 and c["leaves"] > 0 and c["dists"] >= 10 * len(Q)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), ra[0])
+
+
+def _full_properties(P, Q, ids, d2, k):
+    """size-independent checks of a full-size kNN result"""
+    assert (ids < len(P)).all()
+    assert (np.diff(d2, axis=1) >= 0).all()
+    same = np.diff(d2, axis=1) == 0
+    assert (np.diff(ids.astype(np.int64), axis=1)[same] > 0).all()  # ties by ascending id
+    rows = np.random.default_rng(0).choice(len(Q), 20000, replace=False)
+    diff = Q[rows][:, None, :] - P[ids[rows].astype(np.int64)]
+    rec = np.zeros(diff.shape[:2])
+    for j in range(P.shape[1]):
+        rec = rec + diff[..., j] * diff[..., j]
+    assert np.array_equal(rec, d2[rows])
+    return rows
+
+
+@pytest.mark.slow
+def test_full_c2_sampled_against_oracle(gk, oracle):
+    """BASELINE config 2 at full size (10M points, 10M queries): properties on all rows, exact oracle
+    parity on 20k sampled rows (oracle BDL-tree over the same 10M points)."""
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(2)
+    P, (_, Q, k) = script[0][1], script[1]
+    g = gk.BDLTree(3)
+    g.insert(P)
+    ids, d2 = g.knn(Q, k)
+    rows = _full_properties(P, Q, ids, d2, k)
+    o = oracle.BDLTree(3)
+    o.insert(P)
+    assert_struct_equal(g, o, trees=False)
+    assert_tree_equal(g, o, 13)  # the 8.4M-point tree: permutation + nodes bit-exact
+    oi, od = o.knn(Q[rows], k)
+    assert_knn_equal((ids[rows], d2[rows]), (oi, od), "C2 full sampled")
+
+
+@pytest.mark.slow
+def test_full_c1_self_queries(gk, oracle):
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(1)
+    P = script[0][1]
+    g = gk.BDLTree(2)
+    g.insert(P)
+    ids, d2 = g.knn(P, 5)
+    assert np.array_equal(ids[:, 0], np.arange(len(P), dtype=np.uint32)) and (d2[:, 0] == 0).all()
+    rows = _full_properties(P, P, ids, d2, 5)
+    o = oracle.BDLTree(2)
+    o.insert(P)
+    assert_struct_equal(g, o, trees=True)
+    assert_knn_equal((ids[rows], d2[rows]), o.knn(P[rows], 5), "C1 full sampled")
