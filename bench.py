@@ -308,7 +308,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 8,
                     "d2h_bytes_per_step": nq * k * (4 + 8)},
-            "gpu_launches": 7 * args.steps,
+            "gpu_launches": 9 * args.steps,
             "clocks": clk.summary(),
             "build": {"insert_l_points_per_s": built / (build_ms / 1000.0) if build_ms > 0 else None,
                       "build_ms": build_ms, "points": built, "wall_s_incl_ingest": build_wall},

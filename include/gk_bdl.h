@@ -74,6 +74,7 @@ typedef struct gk_bdl_info {
   uint64_t live_per_tree[64];
   uint64_t nodes_per_tree[64];
   int32_t height_per_tree[64];
+  int32_t root_per_tree[64]; /* root slot after Erase_S collapses (-1: emptied) */
 } gk_bdl_info;
 
 typedef struct gk_knn_counters {

@@ -708,6 +708,10 @@ void gko_tree_export(void* h, void* nodes_out, std::uint32_t* ids_out, double* p
   if (ids_out) std::memcpy(ids_out, t->ids.data(), t->n * sizeof(Id));
   if (pts_out) std::memcpy(pts_out, t->pts.data(), t->n * t->d * sizeof(double));
 }
+void gko_tree_dead(void* h, std::uint8_t* out) {
+  auto* t = static_cast<Tree*>(h);
+  if (out && t->n) std::memcpy(out, t->dead.data(), t->n);
+}
 std::uint64_t gko_tree_erase(void* h, const double* P, std::uint64_t n) {
   return erase_static(*static_cast<Tree*>(h), P, n);
 }

@@ -75,6 +75,7 @@ def lib():
         L.gko_tree_free.argtypes = [_P]
         L.gko_tree_info.argtypes = [_P, _P, _P, _P, _P]
         L.gko_tree_export.argtypes = [_P, _P, _P, _P]
+        L.gko_tree_dead.argtypes = [_P, _P]
         L.gko_tree_erase.restype = _u64
         L.gko_tree_erase.argtypes = [_P, _P, _u64]
         L.gko_tree_knn.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
@@ -269,6 +270,20 @@ class BDLTree:
         pts = np.zeros((n, self.d), np.float64)
         lib().gko_tree_export(h, _ptr(nodes), _ptr(ids), _ptr(pts))
         return nodes, ids, pts
+
+    def tree_root(self, i: int) -> int:
+        h = lib().gko_bdl_tree(self.h, i)
+        nn = np.zeros(1, np.uint64); ht = np.zeros(1, np.int32); r = np.zeros(1, np.int32); lv = np.zeros(1, np.uint64)
+        lib().gko_tree_info(h, _ptr(nn), _ptr(ht), _ptr(r), _ptr(lv))
+        return int(r[0])
+
+    def tree_dead(self, i: int) -> np.ndarray:
+        """tombstone flags of static tree i (leaf order)"""
+        h = lib().gko_bdl_tree(self.h, i)
+        n = int(self.stats()["build_size"][i]) if i >= 0 else int(self.stats()["buffer"])
+        out = np.zeros(n, np.uint8)
+        lib().gko_tree_dead(h, _ptr(out))
+        return out.astype(bool)
 
     def live(self):
         n = int(lib().gko_bdl_live(self.h, None, None))

@@ -38,7 +38,8 @@ class GpuError(RuntimeError):
 class _Info(C.Structure):
     _fields_ = [("F", C.c_uint64), ("buffer", C.c_uint64), ("live", C.c_uint64), ("next_id", C.c_uint64),
                 ("build_size", C.c_uint64 * 64), ("live_per_tree", C.c_uint64 * 64),
-                ("nodes_per_tree", C.c_uint64 * 64), ("height_per_tree", C.c_int32 * 64)]
+                ("nodes_per_tree", C.c_uint64 * 64), ("height_per_tree", C.c_int32 * 64),
+                ("root_per_tree", C.c_int32 * 64)]
 
 
 class KnnCounters(C.Structure):
@@ -201,7 +202,8 @@ class BDLTree:
         return dict(F=int(i.F), buffer=int(i.buffer), live=int(i.live), next_id=int(i.next_id),
                     build_size=np.array(i.build_size[:], np.int64), live_per_tree=np.array(i.live_per_tree[:], np.int64),
                     nodes_per_tree=np.array(i.nodes_per_tree[:], np.int64),
-                    height_per_tree=np.array(i.height_per_tree[:], np.int32))
+                    height_per_tree=np.array(i.height_per_tree[:], np.int32),
+                    root_per_tree=np.array(i.root_per_tree[:], np.int32))
 
     def tree_export(self, tree: int):
         """(canonical nodes in vEB order, ids, AoS points) of static tree `tree` or the buffer tree (-1)."""

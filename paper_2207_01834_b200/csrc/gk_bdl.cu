@@ -352,8 +352,11 @@ struct gk_bdl {
     std::uint64_t total = 0;
     for (std::size_t t = 0; t < which.size(); ++t) {
       total += hk[t];
-      if (which[t] >= 0) statics[which[t]].live -= hk[t];
-      else if (hk[t]) {
+      if (which[t] >= 0) {
+        DevTree& T = statics[which[t]];
+        T.live -= hk[t];
+        if (hk[t]) collapse_tree(d, T, st);
+      } else if (hk[t]) {
         // drop the dead buffer points, keeping arrival order, and rebuild the buffer tree
         std::uint32_t* flags = dalloc<std::uint32_t>(buf_n + 1, st);
         std::uint32_t* pos = dalloc<std::uint32_t>(buf_n + 1, st);
@@ -653,6 +656,7 @@ int gk_bdl_info_get(gk_bdl* h, gk_bdl_info* info) {
         info->live_per_tree[i] = h->statics[i].live;
         info->nodes_per_tree[i] = h->statics[i].n_nodes;
         info->height_per_tree[i] = h->statics[i].height;
+        info->root_per_tree[i] = h->statics[i].root_slot;
       }
   });
 }

@@ -426,7 +426,7 @@ __global__ void k_slot_flags(std::uint32_t N, NodeArrays na, std::uint32_t* int_
 
 template <int D>
 __global__ void k_emit(std::uint32_t N, NodeArrays na, const std::uint32_t* __restrict__ irank_by_slot,
-                       gk_canon_node* canon, TNode<D>* tn) {
+                       gk_canon_node* canon, TNode<D>* tn, std::int32_t* orig) {
   std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= N) return;
   const std::uint32_t slot = na.pos[g];
@@ -446,10 +446,16 @@ __global__ void k_emit(std::uint32_t N, NodeArrays na, const std::uint32_t* __re
   }
   if (leaf) {
     c.left = c.right = -1;
+    orig[slot] = -1;
+    orig[N + slot] = -1;
   } else {
     const std::uint32_t cb = na.cbase[g];
     c.left = static_cast<int32_t>(na.pos[cb]);
     c.right = static_cast<int32_t>(na.pos[cb + 1]);
+    orig[slot] = c.left;
+    orig[N + slot] = c.right;
+    orig[2 * N + c.left] = static_cast<std::int32_t>(slot);
+    orig[2 * N + c.right] = static_cast<std::int32_t>(slot);
     TNode<D> t;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -646,24 +652,21 @@ void build_tree_d(int leaf, int heuristic, const double* src, std::uint64_t src_
     const std::uint32_t Sd = lvl_off[d + 1] - lvl_off[d];
     k_veb<<<blocks_for(Sd), 256, 0, st>>>(d, cut[d].first, cut[d].second, d_lvl_off, na);
   }
-  std::uint32_t* int_by_slot = is_int;  // reuse if big enough
-  std::uint32_t* irank_by_slot = irank;
-  bool own = false;
-  if (N + 1 > cap_level + 1) {
-    int_by_slot = dalloc<std::uint32_t>(N + 1, st);
-    irank_by_slot = dalloc<std::uint32_t>(N + 1, st);
-    own = true;
-  }
+  std::uint32_t* int_by_slot = dalloc<std::uint32_t>(N + 1, st);
+  T.irank = dalloc<std::uint32_t>(N + 1, st);
   k_slot_flags<<<blocks_for(N + 1), 256, 0, st>>>(N, na, int_by_slot);
-  scratch.scan(int_by_slot, irank_by_slot, static_cast<std::uint64_t>(N) + 1);
+  scratch.scan(int_by_slot, T.irank, static_cast<std::uint64_t>(N) + 1);
   T.n_internal = (N - 1) / 2;
   T.canon = dalloc<gk_canon_node>(N, st);
   T.tnodes = dalloc<TNode<D>>(T.n_internal, st);
-  k_emit<D><<<blocks_for(N), 256, 0, st>>>(N, na, irank_by_slot, T.canon, static_cast<TNode<D>*>(T.tnodes));
+  T.orig = dalloc<std::int32_t>(3 * static_cast<std::uint64_t>(N), st);
+  GK_CUDA(cudaMemsetAsync(T.orig + 2 * static_cast<std::uint64_t>(N), 0xff, 4, st));  // parent(root) = -1
+  k_emit<D><<<blocks_for(N), 256, 0, st>>>(N, na, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
   GK_CHECK_LAUNCH();
   T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
+  T.root_slot = 0;
 
-  if (own) { dfree(int_by_slot, st); dfree(irank_by_slot, st); }
+  dfree(int_by_slot, st);
   dfree(d_lvl_off, st);
   dfree(bufA, st); dfree(bufB, st); dfree(idsA, st); dfree(idsB, st);
   dfree(na.start, st); dfree(na.count, st); dfree(na.parent, st); dfree(na.cbase, st); dfree(na.nleft, st);
@@ -673,6 +676,81 @@ void build_tree_d(int leaf, int heuristic, const double* src, std::uint64_t src_
   dfree(is_int, st); dfree(irank, st); dfree(obj_list, st); dfree(keys, st); dfree(counters, st);
   dfree(sel, st); dfree(hist, st);
   GK_CUDA(cudaFreeHost(h_counters));
+}
+
+// ------------------------------------------------------------ Erase_S collapse --
+// Bottom-up over the build-time topology (LBVH-refit style: the second child to
+// arrive at a parent computes it).  repl[v] = v if both children survive, the
+// surviving child's replacement if one does, -1 if none; a leaf survives while
+// any of its points is live (tombstone = NaN in coordinate 0).
+__global__ void k_collapse_up(std::uint32_t N, const gk_canon_node* __restrict__ canon, const double* __restrict__ c0,
+                              const std::int32_t* __restrict__ orig, std::int32_t* repl, std::uint32_t* arrive) {
+  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= N || canon[v].kind != 1) return;
+  bool alive = false;
+  for (std::uint32_t i = canon[v].start; i < canon[v].start + canon[v].count; ++i) alive = alive || !isnan(c0[i]);
+  std::int32_t cur = static_cast<std::int32_t>(v);
+  __stcg(&repl[cur], alive ? cur : -1);
+  while (true) {
+    __threadfence();
+    const std::int32_t p = orig[2 * N + cur];
+    if (p < 0) break;
+    if (atomicAdd(&arrive[p], 1u) == 0) break;  // the sibling's thread finishes the parent
+    __threadfence();
+    const std::int32_t a = __ldcg(&repl[orig[p]]), b = __ldcg(&repl[orig[N + p]]);
+    __stcg(&repl[p], (a >= 0 && b >= 0) ? p : (a >= 0 ? a : b));
+    cur = p;
+  }
+}
+
+template <int D>
+__global__ void k_relink(std::uint32_t N, gk_canon_node* canon, TNode<D>* tn, const std::uint32_t* __restrict__ irank,
+                         const std::int32_t* __restrict__ orig, const std::int32_t* __restrict__ repl) {
+  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= N || canon[v].kind != 0) return;
+  const std::int32_t a = repl[orig[v]], b = repl[orig[N + v]];
+  if (a < 0 || b < 0) return;  // v itself is spliced out or removed
+  canon[v].left = a;
+  canon[v].right = b;
+  TNode<D> t = tn[irank[v]];
+  const std::int32_t ch[2] = {a, b};
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const gk_canon_node& c = canon[ch[s]];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      t.lo[s][j] = __double2float_rd(c.lo[j]);
+      t.hi[s][j] = __double2float_ru(c.hi[j]);
+    }
+    t.ref[s] = c.kind == 1 ? make_leaf_ref(c.start, c.count) : static_cast<std::uint64_t>(irank[ch[s]]);
+  }
+  tn[irank[v]] = t;
+}
+
+template <int D>
+void collapse_d(DevTree& T, cudaStream_t st) {
+  const std::uint32_t N = static_cast<std::uint32_t>(T.n_nodes);
+  if (N == 0) return;
+  std::int32_t* repl = dalloc<std::int32_t>(N, st);
+  std::uint32_t* arrive = dalloc<std::uint32_t>(N, st);
+  GK_CUDA(cudaMemsetAsync(arrive, 0, static_cast<std::size_t>(N) * 4, st));
+  k_collapse_up<<<blocks_for(N), 256, 0, st>>>(N, T.canon, T.coords, T.orig, repl, arrive);
+  k_relink<D><<<blocks_for(N), 256, 0, st>>>(N, T.canon, static_cast<TNode<D>*>(T.tnodes), T.irank, T.orig, repl);
+  GK_CHECK_LAUNCH();
+  std::int32_t root = -1;
+  gk_canon_node rc;
+  GK_CUDA(cudaMemcpyAsync(&root, repl, 4, cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  T.root_slot = root;
+  if (root >= 0) {
+    std::uint32_t ir = 0;
+    GK_CUDA(cudaMemcpyAsync(&rc, T.canon + root, sizeof(rc), cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaMemcpyAsync(&ir, T.irank + root, 4, cudaMemcpyDeviceToHost, st));
+    GK_CUDA(cudaStreamSynchronize(st));
+    T.root_ref = rc.kind == 1 ? make_leaf_ref(rc.start, rc.count) : ir;
+  }
+  dfree(repl, st);
+  dfree(arrive, st);
 }
 
 }  // namespace
@@ -691,12 +769,27 @@ void build_tree(int d, int leaf, int heuristic, const double* src, std::uint64_t
   }
 }
 
+void collapse_tree(int d, DevTree& t, cudaStream_t st) {
+  switch (d) {
+    case 2: collapse_d<2>(t, st); break;
+    case 3: collapse_d<3>(t, st); break;
+    case 4: collapse_d<4>(t, st); break;
+    case 5: collapse_d<5>(t, st); break;
+    case 6: collapse_d<6>(t, st); break;
+    case 7: collapse_d<7>(t, st); break;
+    case 8: collapse_d<8>(t, st); break;
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
 void free_tree(DevTree& t, cudaStream_t st) {
   dfree(t.coords, st);
   dfree(t.ids, st);
   if (t.tnodes) GK_CUDA(cudaFreeAsync(t.tnodes, st));
   t.tnodes = nullptr;
   dfree(t.canon, st);
+  dfree(t.orig, st);
+  dfree(t.irank, st);
   t = DevTree();
 }
 

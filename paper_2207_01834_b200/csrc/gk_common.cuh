@@ -70,6 +70,9 @@ struct DevTree {
   std::uint64_t root_ref = 0;
   gk_canon_node* canon = nullptr; // canonical nodes, vEB slot order
   std::uint64_t n_nodes = 0;
+  std::int32_t* orig = nullptr;   // build-time topology per slot: [left | right | parent] (3 x n_nodes)
+  std::uint32_t* irank = nullptr; // slot -> internal rank (TNode index), n_nodes + 1
+  std::int32_t root_slot = 0;     // -1 once Erase_S removed every point
   int height = 0;
   std::uint64_t build_size = 0, live = 0;
 };
@@ -92,6 +95,10 @@ struct TreeSet {
 void build_tree(int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st);
 void free_tree(DevTree& t, cudaStream_t st);
+// Erase_S collapse: after tombstoning, drop emptied leaves
+// and splice out internal nodes left with one child; relinks the canonical
+// nodes and the traversal nodes and updates root_slot / root_ref.
+void collapse_tree(int d, DevTree& t, cudaStream_t st);
 
 // knn.cu
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq,

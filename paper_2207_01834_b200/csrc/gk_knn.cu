@@ -38,45 +38,47 @@ __device__ __forceinline__ bool lexlt(double a, std::uint32_t ia, double b, std:
   return a < b || (a == b && ia < ib);
 }
 
+// Sorted insertion of (x, id) into the register top-K (x is known to beat slot K-1).
+// Slot j takes slot j-1 when x precedes it, x itself when x precedes slot j but
+// not slot j-1, else keeps its value; each comparison is made once.
 template <int K>
 __device__ __forceinline__ void insert_cand(double x, std::uint32_t id, double (&cd)[K], std::uint32_t (&ci)[K]) {
-  if (!lexlt(x, id, cd[K - 1], ci[K - 1])) return;
+  bool after = true;  // x precedes the (old) value of slot j
 #pragma unroll
   for (int j = K - 1; j > 0; --j) {
-    if (lexlt(x, id, cd[j - 1], ci[j - 1])) {
-      cd[j] = cd[j - 1];
-      ci[j] = ci[j - 1];
-    } else if (lexlt(x, id, cd[j], ci[j])) {
-      cd[j] = x;
-      ci[j] = id;
-    }
+    const bool before = lexlt(x, id, cd[j - 1], ci[j - 1]);
+    const double v = before ? cd[j - 1] : (after ? x : cd[j]);
+    const std::uint32_t vi = before ? ci[j - 1] : (after ? id : ci[j]);
+    cd[j] = v;
+    ci[j] = vi;
+    after = before;
   }
-  if (lexlt(x, id, cd[0], ci[0])) {
+  if (after) {
     cd[0] = x;
     ci[0] = id;
   }
 }
 
-// lower bound of the canonical d2 of any point inside [lo, hi] (same op order)
+// fp32 lower bound of the canonical fp64 d2 of every point inside the box
+// [lo, hi]: per-dimension gaps rounded down from (q rounded out), squares and
+// sums rounded down, then scaled by (1 - 2^-23) rounded down so that it stays
+// below the fp64 rounding of the true d2 (relative error <= (D+1) 2^-53).
 template <int D>
-__device__ __forceinline__ double box_mindist(const double (&q)[D], const float* lo, const float* hi) {
-  double s = 0.0;
+__device__ __forceinline__ float box_lb(const float (&qlo)[D], const float (&qhi)[D], const float* lo, const float* hi) {
+  float s = 0.f;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    const double l = static_cast<double>(lo[j]), h = static_cast<double>(hi[j]);
-    double t = 0.0;
-    if (q[j] < l) t = __dsub_rn(l, q[j]);
-    else if (q[j] > h) t = __dsub_rn(q[j], h);
-    s = __dadd_rn(s, __dmul_rn(t, t));
+    const float t = fmaxf(fmaxf(__fsub_rd(lo[j], qhi[j]), __fsub_rd(qlo[j], hi[j])), 0.f);
+    s = __fadd_rd(s, __fmul_rd(t, t));
   }
-  return s;
+  return __fmul_rd(s, 0x1.fffffcp-1f);
 }
 
-template <int D, int K>
-__global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const double* __restrict__ Q,
-                                                     const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
-                                                     std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
-                                                     unsigned long long* __restrict__ counters) {
+template <int D, int K, bool COUNT>
+__global__ void __launch_bounds__(kWarps * 32, 3) k_knn(const TreeSet ts, const double* __restrict__ Q,
+                                                        const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
+                                                        std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
+                                                        unsigned long long* __restrict__ counters) {
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
@@ -87,6 +89,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
   const bool active = qi < nq;
   std::uint32_t orig = 0;
   double q[D];
+  float qlo[D], qhi[D];
   if (active) {
     orig = perm ? perm[qi] : static_cast<std::uint32_t>(qi);
 #pragma unroll
@@ -95,6 +98,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
 #pragma unroll
     for (int j = 0; j < D; ++j) q[j] = 0.0;
   }
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    qlo[j] = __double2float_rd(q[j]);
+    qhi[j] = __double2float_ru(q[j]);
+  }
   double cd[K];
   std::uint32_t ci[K];
 #pragma unroll
@@ -102,12 +110,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
     cd[j] = __longlong_as_double(0x7ff0000000000000LL);  // +inf, kNoPoint: KnnBuffer's initial bound
     ci[j] = GK_NO_POINT;
   }
+  // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
+  float kthf = active ? __int_as_float(0x7f800000) : -1.f;
   float mdst[kStack];
-  const bool count = counters != nullptr;
   unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0;
 
   for (int t = 0; t < ts.count; ++t) {
-    const TNode<D>* __restrict__ nodes = static_cast<const TNode<D>*>(ts.t[t].tnodes);
+    const float4* __restrict__ nodes = static_cast<const float4*>(ts.t[t].tnodes);
     const double* __restrict__ coords = ts.t[t].coords;
     const std::uint32_t* __restrict__ ids = ts.t[t].ids;
     const std::uint64_t stride = ts.t[t].stride;
@@ -125,38 +134,47 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
           s_ids[w][lane] = ids[s + lane];
         }
         __syncwarp();
-        if (active) {
-          for (std::uint32_t p = 0; p < c; ++p) {
-            double d2 = 0.0;
+        for (std::uint32_t p = 0; p < c; ++p) {
+          const double t0 = __dsub_rn(q[0], s_pts[w][p]);
+          double d2 = __dmul_rn(t0, t0);  // 0 + t0^2 == t0^2 exactly
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-              const double tt = __dsub_rn(q[j], s_pts[w][j * GK_MAX_LEAF + p]);
-              d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
-            }
-            insert_cand<K>(d2, s_ids[w][p], cd, ci);
+          for (int j = 1; j < D; ++j) {
+            const double tt = __dsub_rn(q[j], s_pts[w][j * GK_MAX_LEAF + p]);
+            d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
+          }
+          const std::uint32_t pid = s_ids[w][p];
+          if (lexlt(d2, pid, cd[K - 1], ci[K - 1])) {
+            insert_cand<K>(d2, pid, cd, ci);
+            kthf = __double2float_ru(cd[K - 1]);
           }
         }
-        if (count) {
+        if (COUNT) {
           if (need) { c_leaves++; c_dists += c; }
           c_wl++;
         }
       } else {
-        const TNode<D>& nd = nodes[ref];
-        float lo0[D], hi0[D], lo1[D], hi1[D];
+        const float4* nd = nodes + ref * (D + 1);
+        float lo0[D], lo1[D], hi0[D], hi1[D];
+        {
+          float f[4 * D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          lo0[j] = nd.lo[0][j]; hi0[j] = nd.hi[0][j];
-          lo1[j] = nd.lo[1][j]; hi1[j] = nd.hi[1][j];
+          for (int v = 0; v < D; ++v) {
+            const float4 x = nd[v];
+            f[4 * v] = x.x; f[4 * v + 1] = x.y; f[4 * v + 2] = x.z; f[4 * v + 3] = x.w;
+          }
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            lo0[j] = f[j]; lo1[j] = f[D + j]; hi0[j] = f[2 * D + j]; hi1[j] = f[3 * D + j];
+          }
         }
-        const std::uint64_t r0 = nd.ref[0], r1 = nd.ref[1];
-        if (count) {
+        const ulonglong2 rr = *reinterpret_cast<const ulonglong2*>(nd + D);
+        if (COUNT) {
           if (need) c_nodes++;
           c_wn++;
         }
-        const double m0 = box_mindist<D>(q, lo0, hi0);
-        const double m1 = box_mindist<D>(q, lo1, hi1);
-        const double kth = cd[K - 1];
-        const bool w0 = active && m0 <= kth, w1 = active && m1 <= kth;
+        const float m0 = box_lb<D>(qlo, qhi, lo0, hi0);
+        const float m1 = box_lb<D>(qlo, qhi, lo1, hi1);
+        const bool w0 = m0 <= kthf, w1 = m1 <= kthf;
         const unsigned b0 = __ballot_sync(0xffffffffu, w0), b1 = __ballot_sync(0xffffffffu, w1);
         if (b0 && b1) {
           // near child first, by majority of the lanes that want both (else by lane count)
@@ -168,19 +186,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
           } else {
             first = (__popc(b0) >= __popc(b1)) ? 0 : 1;
           }
-          const std::uint64_t rs = first ? r0 : r1;
-          const double ms = first ? m0 : m1;
-          if (lane == 0) s_stack[w][sp] = rs;
-          mdst[sp] = active ? __double2float_rd(ms) : __int_as_float(0x7f800000);
+          if (lane == 0) s_stack[w][sp] = first ? rr.x : rr.y;
+          mdst[sp] = first ? m0 : m1;
           ++sp;
-          ref = first ? r1 : r0;
+          ref = first ? rr.y : rr.x;
           need = first ? w1 : w0;
           continue;
         } else if (b0) {
-          ref = r0; need = w0;
+          ref = rr.x; need = w0;
           continue;
         } else if (b1) {
-          ref = r1; need = w1;
+          ref = rr.y; need = w1;
           continue;
         }
       }
@@ -189,7 +205,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
       __syncwarp();
       while (sp > 0) {
         --sp;
-        const bool nl = active && static_cast<double>(mdst[sp]) <= cd[K - 1];
+        const bool nl = mdst[sp] <= kthf;
         if (__any_sync(0xffffffffu, nl)) {
           ref = s_stack[w][sp];
           need = nl;
@@ -209,9 +225,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_knn(const TreeSet ts, const dou
         out_d2[static_cast<std::uint64_t>(orig) * k + j] = cd[j];
       }
   }
-  if (count) {
+  if (COUNT) {
     const unsigned long long node_b = sizeof(TNode<D>), pt_b = 8 * D + 4;
-    unsigned long long v[5] = {c_nodes, c_leaves, c_dists, 0, 0};
+    unsigned long long v[3] = {c_nodes, c_leaves, c_dists};
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -286,7 +302,8 @@ template <int D, int K>
 void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, int k, std::uint32_t* ids,
               double* d2, unsigned long long* ctr, cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
-  k_knn<D, K><<<blocks, kWarps * 32, 0, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
+  if (ctr) k_knn<D, K, true><<<blocks, kWarps * 32, 0, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
+  else k_knn<D, K, false><<<blocks, kWarps * 32, 0, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
 }
 
 template <int D>

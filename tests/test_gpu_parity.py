@@ -30,10 +30,25 @@ def assert_tree_equal(g, o, i):
     gn, gi, gp = g.tree_export(i)
     on, oi, op = o.tree_export(i)
     assert np.array_equal(gi, oi), f"tree {i}: permutation differs"
-    np.testing.assert_array_equal(gp, op)
+    dead = o.tree_dead(i)  # the device tombstone is a NaN in coordinate 0
+    assert np.array_equal(np.isnan(gp[:, 0]), dead), f"tree {i}: tombstones differ"
+    np.testing.assert_array_equal(gp[~dead], op[~dead])
+    np.testing.assert_array_equal(gp[dead, 1:], op[dead, 1:])
     assert len(gn) == len(on), f"tree {i}: {len(gn)} vs {len(on)} nodes"
+    groot, oroot = int(g.info()["root_per_tree"][i]), o.tree_root(i)
+    assert groot == oroot, f"tree {i}: root slot {groot} vs {oroot}"
+    # nodes reachable from the root (Erase_S collapses splice nodes out; unreachable records are stale)
+    reach, stack = [], [groot] if groot >= 0 else []
+    while stack:
+        v = stack.pop()
+        reach.append(v)
+        if on[v]["kind"] == 0:
+            stack += [int(on[v]["right"]), int(on[v]["left"])]
+    reach = np.array(reach, np.int64)
+    if not dead.any():
+        assert len(reach) == len(on)
     for f in FIELDS:
-        assert np.array_equal(gn[f], on[f]), f"tree {i}: node field {f} differs"
+        assert np.array_equal(gn[f][reach], on[f][reach]), f"tree {i}: node field {f} differs"
 
 
 def assert_struct_equal(g, o, trees=True):
