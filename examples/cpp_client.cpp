@@ -1,0 +1,24 @@
+// Minimal C++ client of include/geokit_bdl.hpp (what a reference-side caller,
+// e.g. the absent `knn` CLI subcommand of SPEC.md:660-663, would write).
+//   g++ -std=c++20 -Iinclude examples/cpp_client.cpp -Lpaper_2207_01834_b200/_lib -lgkbdl
+//       -Wl,-rpath,$PWD/paper_2207_01834_b200/_lib -o /tmp/cpp_client && /tmp/cpp_client
+#include <array>
+#include <cstdio>
+#include <vector>
+
+#include "geokit_bdl.hpp"
+
+int main() {
+  std::vector<std::array<double, 3>> P(100000);
+  if (gk_gen_uniform(P.size(), 3, 2, P[0].data()) != GK_OK) return 1;
+  geokit::bdltree::BDLTree<3> tree;           // X = 1024, leaf 16, spatial median
+  tree.insert(P);                             // bdl_build
+  auto nn = tree.knn(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 4), 3);
+  for (auto& row : nn) {
+    for (auto& [d2, id] : row) std::printf("(%u, %.3g) ", id, d2);
+    std::printf("\n");
+  }
+  const unsigned long long erased = tree.erase(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 10));
+  std::printf("erased %llu, live %llu\n", erased, (unsigned long long)tree.size());
+  return 0;
+}

@@ -75,13 +75,18 @@ __device__ __forceinline__ float box_lb(const float (&qlo)[D], const float (&qhi
 }
 
 template <int D, int K, bool COUNT>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_knn(const TreeSet ts, const double* __restrict__ Q,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
                                                         unsigned long long* __restrict__ counters) {
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
+  // per-lane sorted top-K, one column per thread (conflict-free): [K][blockDim] d2, then [K][blockDim] ids
+  extern __shared__ double s_cand[];
+  double* cdv = s_cand + threadIdx.x;
+  std::uint32_t* civ = reinterpret_cast<std::uint32_t*>(s_cand + K * kWarps * 32) + threadIdx.x;
+  constexpr int CS = kWarps * 32;  // column stride
 
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
@@ -103,13 +108,14 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_knn(const TreeSet ts, const 
     qlo[j] = __double2float_rd(q[j]);
     qhi[j] = __double2float_ru(q[j]);
   }
-  double cd[K];
-  std::uint32_t ci[K];
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    cd[j] = __longlong_as_double(0x7ff0000000000000LL);  // +inf, kNoPoint: KnnBuffer's initial bound
-    ci[j] = GK_NO_POINT;
+    cdv[j * CS] = kInf;  // (+inf, kNoPoint): KnnBuffer's initial bound
+    civ[j * CS] = GK_NO_POINT;
   }
+  double kd = kInf;                 // current k-th (d2, id)
+  std::uint32_t kid = GK_NO_POINT;
   // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
   float kthf = active ? __int_as_float(0x7f800000) : -1.f;
   float mdst[kStack];
@@ -142,10 +148,24 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_knn(const TreeSet ts, const 
             const double tt = __dsub_rn(q[j], s_pts[w][j * GK_MAX_LEAF + p]);
             d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
           }
-          const std::uint32_t pid = s_ids[w][p];
-          if (lexlt(d2, pid, cd[K - 1], ci[K - 1])) {
-            insert_cand<K>(d2, pid, cd, ci);
-            kthf = __double2float_ru(cd[K - 1]);
+          if (d2 <= kd) {  // rare: lexicographic test, then sorted insertion with early exit
+            const std::uint32_t pid = s_ids[w][p];
+            if (d2 < kd || pid < kid) {
+              int j = K - 1;
+              while (j > 0) {
+                const double cv = cdv[(j - 1) * CS];
+                const std::uint32_t cid = civ[(j - 1) * CS];
+                if (!lexlt(d2, pid, cv, cid)) break;
+                cdv[j * CS] = cv;
+                civ[j * CS] = cid;
+                --j;
+              }
+              cdv[j * CS] = d2;
+              civ[j * CS] = pid;
+              kd = cdv[(K - 1) * CS];
+              kid = civ[(K - 1) * CS];
+              kthf = __double2float_ru(kd);
+            }
           }
         }
         if (COUNT) {
@@ -221,8 +241,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_knn(const TreeSet ts, const 
 #pragma unroll
     for (int j = 0; j < K; ++j)
       if (j < k) {
-        out_ids[static_cast<std::uint64_t>(orig) * k + j] = ci[j];
-        out_d2[static_cast<std::uint64_t>(orig) * k + j] = cd[j];
+        out_ids[static_cast<std::uint64_t>(orig) * k + j] = civ[j * CS];
+        out_d2[static_cast<std::uint64_t>(orig) * k + j] = cdv[j * CS];
       }
   }
   if (COUNT) {
@@ -302,8 +322,15 @@ template <int D, int K>
 void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, int k, std::uint32_t* ids,
               double* d2, unsigned long long* ctr, cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
-  if (ctr) k_knn<D, K, true><<<blocks, kWarps * 32, 0, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
-  else k_knn<D, K, false><<<blocks, kWarps * 32, 0, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
+  const int smem = K * kWarps * 32 * 12;  // per-lane top-K columns
+  static bool configured = false;  // per (D, K) instantiation
+  if (!configured) {
+    GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  if (ctr) k_knn<D, K, true><<<blocks, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
+  else k_knn<D, K, false><<<blocks, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
 }
 
 template <int D>

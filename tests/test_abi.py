@@ -41,3 +41,19 @@ def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def _compile_client(out):
+    import subprocess
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    lib = os.path.join(ROOT, "paper_2207_01834_b200", "_lib")
+    r = subprocess.run([cxx, "-std=c++20", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "cpp_client.cpp"), "-L", lib, "-lgkbdl",
+                        f"-Wl,-rpath,{lib}", "-o", out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_cpp_binding_compiles(gk, tmp_path):
+    """include/geokit_bdl.hpp (the reference-side C++ binding) compiles and links against the ABI"""
+    _compile_client(str(tmp_path / "client"))
