@@ -65,20 +65,35 @@ __device__ __forceinline__ void insert_cand(double x, std::uint32_t id, double (
 // below the fp64 rounding of the true d2 (relative error <= (D+1) 2^-53).
 template <int D>
 __device__ __forceinline__ float box_lb(const float (&qlo)[D], const float (&qhi)[D], const float* lo, const float* hi) {
-  float s = 0.f;
+  const float t0 = fmaxf(fmaxf(__fsub_rd(lo[0], qhi[0]), __fsub_rd(qlo[0], hi[0])), 0.f);
+  float s = __fmul_rd(t0, t0);
 #pragma unroll
-  for (int j = 0; j < D; ++j) {
+  for (int j = 1; j < D; ++j) {
     const float t = fmaxf(fmaxf(__fsub_rd(lo[j], qhi[j]), __fsub_rd(qlo[j], hi[j])), 0.f);
     s = __fadd_rd(s, __fmul_rd(t, t));
   }
   return __fmul_rd(s, 0x1.fffffcp-1f);
 }
 
+// distance of the query to staged leaf point p (canonical order, no FMA)
+template <int D>
+__device__ __forceinline__ double leaf_d2(const double (&q)[D], const double* sp, int p) {
+  const double t0 = __dsub_rn(q[0], sp[p]);
+  double d2 = __dmul_rn(t0, t0);  // 0 + t0^2 == t0^2 exactly
+#pragma unroll
+  for (int j = 1; j < D; ++j) {
+    const double tt = __dsub_rn(q[j], sp[j * GK_MAX_LEAF + p]);
+    d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
+  }
+  return d2;
+}
+
 template <int D, int K, bool COUNT>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
-                                                        unsigned long long* __restrict__ counters) {
+                                                        unsigned long long* __restrict__ counters,
+                                                        unsigned* __restrict__ tile_ctr) {
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
@@ -90,7 +105,19 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const 
 
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const std::uint64_t qi = (static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+  const unsigned ntiles = static_cast<unsigned>((nq + 31) / 32);
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0;
+  float mdst[kStack];
+
+  // persistent warps: each grabs the next 32-query tile (Morton order keeps
+  // concurrently processed tiles adjacent, so their trees' paths share L1/L2)
+  while (true) {
+  unsigned tile = 0;
+  if (lane == 0) tile = atomicAdd(tile_ctr, 1u);
+  tile = __shfl_sync(0xffffffffu, tile, 0);
+  if (tile >= ntiles) break;
+  const std::uint64_t qi = static_cast<std::uint64_t>(tile) * 32 + lane;
   const bool active = qi < nq;
   std::uint32_t orig = 0;
   double q[D];
@@ -108,7 +135,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const 
     qlo[j] = __double2float_rd(q[j]);
     qhi[j] = __double2float_ru(q[j]);
   }
-  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     cdv[j * CS] = kInf;  // (+inf, kNoPoint): KnnBuffer's initial bound
@@ -118,8 +144,27 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const 
   std::uint32_t kid = GK_NO_POINT;
   // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
   float kthf = active ? __int_as_float(0x7f800000) : -1.f;
-  float mdst[kStack];
-  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0;
+
+  auto offer = [&](double d2, std::uint32_t pid) {
+    if (d2 <= kd) {  // rare: lexicographic test, then sorted insertion with early exit
+      if (d2 < kd || pid < kid) {
+        int j = K - 1;
+        while (j > 0) {
+          const double cv = cdv[(j - 1) * CS];
+          const std::uint32_t cid = civ[(j - 1) * CS];
+          if (!lexlt(d2, pid, cv, cid)) break;
+          cdv[j * CS] = cv;
+          civ[j * CS] = cid;
+          --j;
+        }
+        cdv[j * CS] = d2;
+        civ[j * CS] = pid;
+        kd = cdv[(K - 1) * CS];
+        kid = civ[(K - 1) * CS];
+        kthf = __double2float_ru(kd);
+      }
+    }
+  };
 
   for (int t = 0; t < ts.count; ++t) {
     const float4* __restrict__ nodes = static_cast<const float4*>(ts.t[t].tnodes);
@@ -138,35 +183,16 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const 
 #pragma unroll
           for (int j = 0; j < D; ++j) s_pts[w][j * GK_MAX_LEAF + lane] = coords[j * stride + s + lane];
           s_ids[w][lane] = ids[s + lane];
+        } else if (lane == static_cast<int>(c) && (c & 1u)) {
+          s_pts[w][lane] = __longlong_as_double(0x7ff8000000000000LL);  // NaN pad: never enters the top-k
         }
         __syncwarp();
-        for (std::uint32_t p = 0; p < c; ++p) {
-          const double t0 = __dsub_rn(q[0], s_pts[w][p]);
-          double d2 = __dmul_rn(t0, t0);  // 0 + t0^2 == t0^2 exactly
-#pragma unroll
-          for (int j = 1; j < D; ++j) {
-            const double tt = __dsub_rn(q[j], s_pts[w][j * GK_MAX_LEAF + p]);
-            d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
-          }
-          if (d2 <= kd) {  // rare: lexicographic test, then sorted insertion with early exit
-            const std::uint32_t pid = s_ids[w][p];
-            if (d2 < kd || pid < kid) {
-              int j = K - 1;
-              while (j > 0) {
-                const double cv = cdv[(j - 1) * CS];
-                const std::uint32_t cid = civ[(j - 1) * CS];
-                if (!lexlt(d2, pid, cv, cid)) break;
-                cdv[j * CS] = cv;
-                civ[j * CS] = cid;
-                --j;
-              }
-              cdv[j * CS] = d2;
-              civ[j * CS] = pid;
-              kd = cdv[(K - 1) * CS];
-              kid = civ[(K - 1) * CS];
-              kthf = __double2float_ru(kd);
-            }
-          }
+        // two independent distance chains per iteration (fp64 latency)
+        for (std::uint32_t p = 0; p < c; p += 2) {
+          const double da = leaf_d2<D>(q, s_pts[w], p);
+          const double db = leaf_d2<D>(q, s_pts[w], p + 1);
+          offer(da, s_ids[w][p]);
+          offer(db, s_ids[w][p + 1]);
         }
         if (COUNT) {
           if (need) { c_leaves++; c_dists += c; }
@@ -245,6 +271,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const 
         out_d2[static_cast<std::uint64_t>(orig) * k + j] = cdv[j * CS];
       }
   }
+  }  // tile loop
+
   if (COUNT) {
     const unsigned long long node_b = sizeof(TNode<D>), pt_b = 8 * D + 4;
     unsigned long long v[3] = {c_nodes, c_leaves, c_dists};
@@ -329,8 +357,21 @@ void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std
     GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  if (ctr) k_knn<D, K, true><<<blocks, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
-  else k_knn<D, K, false><<<blocks, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr);
+  static int resident = 0;  // blocks per SM at this smem size
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    GK_CUDA(cudaGetDevice(&dev));
+    GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn<D, K, false>, kWarps * 32, smem));
+    resident = std::max(1, per) * sms;
+  }
+  const unsigned grid = std::min<unsigned>(blocks, static_cast<unsigned>(resident));
+  unsigned* tile_ctr = nullptr;
+  GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
+  GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
+  if (ctr) k_knn<D, K, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
+  else k_knn<D, K, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
+  GK_CUDA(cudaFreeAsync(tile_ctr, st));
 }
 
 template <int D>
