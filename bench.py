@@ -206,13 +206,22 @@ def run_gpu(args):
     nq = len(Q)
     g = gk.BDLTree(d, device=dev.index)
 
-    # ---- build (Insert_L / BuildvEB_S), device-resident input
+    # ---- build (Insert_L / BuildvEB_S), device-resident input: 1 cold + 3 warm Insert_L into fresh handles
     P_dev = torch.from_numpy(P).to(dev)
     torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    g.insert_device(P_dev)
-    build_wall = time.perf_counter() - t0
-    build_ms, built = g.last_build_ms()
+    build_runs = []
+    for rep in range(4):
+        if rep:
+            g.close()
+            g = gk.BDLTree(d, device=dev.index)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        g.insert_device(P_dev)
+        wall = time.perf_counter() - t0
+        bms, built = g.last_build_ms()
+        build_runs.append((wall, bms))
+    build_wall = min(w for w, _ in build_runs[1:])
+    build_ms = min(b for _, b in build_runs[1:])
     del P_dev
 
     Q_dev = torch.from_numpy(Q).to(dev)
@@ -245,12 +254,9 @@ def run_gpu(args):
             step_ms.append(e0.elapsed_time(e1))
             trav_ms.append(g.last_knn_ms()[0])
     torch.cuda.synchronize(dev)
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * nq * args.steps / (total_ms / 1000.0)
+    from paper_2207_01834_b200.replicas import max_over_ranks, whole_job_rate
+    total_ms = max_over_ranks(sum(step_ms), device=dev)
+    value = whole_job_rate(nq * args.steps, world, total_ms / 1000.0)
 
     # ---- e2e through the public host API (pinned host buffers, H2D + D2H inside the timed region)
     Qh = torch.from_numpy(Q).pin_memory().numpy()
@@ -265,12 +271,8 @@ def run_gpu(args):
         torch.cuda.synchronize(dev)
         e2e_s.append(time.perf_counter() - t0)
         assert rc == 0, gk.lib().gk_last_error()
-    e2e_t = sum(e2e_s)
-    if world > 1:
-        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_t = float(t.item())
-    e2e = world * nq * len(e2e_s) / e2e_t
+    e2e_t = max_over_ranks(sum(e2e_s), device=dev)
+    e2e = whole_job_rate(nq * len(e2e_s), world, e2e_t)
 
     if rank == 0:
         hbm, peak_src = measured_peaks()
@@ -310,8 +312,11 @@ def run_gpu(args):
                     "d2h_bytes_per_step": nq * k * (4 + 8)},
             "gpu_launches": 9 * args.steps,
             "clocks": clk.summary(),
-            "build": {"insert_l_points_per_s": built / (build_ms / 1000.0) if build_ms > 0 else None,
-                      "build_ms": build_ms, "points": built, "wall_s_incl_ingest": build_wall},
+            "build": {"insert_l_points_per_s": len(P) / build_wall, "buildveb_points_per_s": built / (build_ms / 1000.0),
+                      "insert_l_ms": 1000 * build_wall, "buildveb_ms": build_ms, "points": built,
+                      "cold_insert_l_ms": 1000 * build_runs[0][0],
+                      "note": "Insert_L of all points into a fresh handle (device-resident input, ingest+validation "
+                              "included), best of 3 warm runs; buildveb_ms = device time of the tree builds"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
