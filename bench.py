@@ -127,8 +127,6 @@ def config_inputs(cfg: int, scale: float):
     d, script = make_inputs(cfg, scale)
     P = [op[1] for op in script if op[0] == "insert"]
     K = [op for op in script if op[0] == "knn"]
-    if cfg != 2 and cfg != 1 and cfg != 3:
-        raise SystemExit("bench.py measures the single-insert configs (1, 2, 3); configs 4/5 are parity cases")
     return d, P[0], K[0][1], K[0][2]
 
 
@@ -323,10 +321,55 @@ def run_gpu(args):
         torch.distributed.destroy_process_group()
 
 
+def run_script(args):
+    """Configs 4/5 (dynamic scripts): replay the whole Insert_L / Erase_L / kNN_L script
+    on the device (inputs pre-staged in HBM); value = kNN_L queries/s over all kNN ops."""
+    import torch
+    import paper_2207_01834_b200 as gk
+    from paper_2207_01834_b200.configs import CONFIGS, make_inputs
+    rank, world, _ = dist_env()
+    dev = torch.device("cuda", 0)
+    d, script = make_inputs(args.config, args.scale)
+    staged = [(op[0], torch.from_numpy(op[1]).to(dev)) + tuple(op[2:]) for op in script]
+    res = {}
+    for rep in range(2):  # rep 0 warms the memory pool
+        g = gk.BDLTree(d)
+        t = {"insert": [0, 0.0], "erase": [0, 0.0], "knn": [0, 0.0]}
+        for op in staged:
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            if op[0] == "insert":
+                g.insert_device(op[1])
+            elif op[0] == "erase":
+                g.erase_device(op[1])
+            else:
+                k = op[2]
+                ids = torch.empty((op[1].shape[0], k), dtype=torch.int32, device=dev)
+                d2 = torch.empty((op[1].shape[0], k), dtype=torch.float64, device=dev)
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                g.knn_device(op[1], k, ids, d2)
+            torch.cuda.synchronize(dev)
+            t[op[0]][0] += op[1].shape[0]
+            t[op[0]][1] += time.perf_counter() - t0
+        res = t
+        g.close()
+    line = {"metric": "kNN_L queries/s", "value": res["knn"][0] / res["knn"][1], "unit": "queries/s", "n_gpus": 1,
+            "steps": 1, "warmup": 1, "ms_per_step": 1000 * sum(v[1] for v in res.values()), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config]["name"], "scale": args.scale},
+            "insert_l_points_per_s": res["insert"][0] / res["insert"][1] if res["insert"][1] else None,
+            "erase_l_points_per_s": res["erase"][0] / res["erase"][1] if res["erase"][1] else None,
+            "ops_seconds": {k: v[1] for k, v in res.items()}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config in (4, 5):
+        run_script(args)
     else:
         run_gpu(args)
 

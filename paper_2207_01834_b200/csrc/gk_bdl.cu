@@ -190,6 +190,7 @@ struct gk_bdl {
   std::uint64_t built_pts = 0;
   void* cub_tmp = nullptr;
   std::size_t cub_bytes = 0;
+  BuildScratch scratch;
 
   std::uint64_t bstride() const { return 2ULL * X; }
 
@@ -225,7 +226,7 @@ struct gk_bdl {
     // build over arrival indices, then map them to ids (keeping the map for erase)
     std::uint32_t* iota = dalloc<std::uint32_t>(buf_n, st);
     k_iota<<<blocks_for(buf_n), 256, 0, st>>>(iota, buf_n);
-    build_tree(d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), iota, buf_n, buf_tree, st);
+    build_tree(scratch, d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), iota, buf_n, buf_tree, st);
     buf_src = dalloc<std::uint32_t>(buf_n, st);
     k_gather_ids<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_src, buf_ids, buf_n);
     GK_CHECK_LAUNCH();
@@ -294,7 +295,7 @@ struct gk_bdl {
         F &= ~(1ULL << i);
         continue;
       }
-      build_tree(d, static_cast<int>(leaf), heuristic, pool + o, pool_n, pool_ids + o, c, statics[i], st);
+      build_tree(scratch, d, static_cast<int>(leaf), heuristic, pool + o, pool_n, pool_ids + o, c, statics[i], st);
       o += c;
       built_pts_now += c;
     }

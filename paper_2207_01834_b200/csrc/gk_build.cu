@@ -1,38 +1,49 @@
-// gk_build.cu — BuildvEB_S on the B200 (sm_100a): a level-synchronous pipeline.
+// gk_build.cu — BuildvEB_S on the B200 (sm_100a): one persistent cooperative
+// kernel per tree; every level of the build runs inside it, separated by
+// grid-wide barriers, so no level ever returns to the host.
 //
 // Reference semantics (restated; the reference ships no code for it):
 //   PAPER.md:1110-1127 Alg. 1 BuildvEB_S, 1141-1146 recursion, 1484-1487 spatial
 //   median = (min+max)/2, 1491 leaf 16.
-// Frozen decisions (DESIGN.md §Frozen, mirrored by oracle/gk_oracle.cpp):
+// Frozen decisions (DESIGN.md §2, mirrored by oracle/gk_oracle.cpp):
 //   split dim = depth mod D; spatial split s = (lo+hi)/2, left x_c < s <= right;
 //   stable partition; degenerate side or depth >= 40 or heuristic = object ->
 //   object median by (x_c, id), left = the floor(n/2) smallest keys; leaf when
 //   n <= leaf; vEB layout topology-driven (complete-tree vEB order restricted
 //   to the nodes that exist).
 //
-// Device pipeline per level L (all nodes of the level at once, any number of trees' worth of segments):
-//   chunking   -> each node's point range is cut into <=1024-point chunks, one warp per chunk
-//   k_bbox     -> per-node bounding box: coalesced fp64 loads, warp min/max, one atomic per chunk
-//   k_split    -> node record: leaf / spatial split / object-median flag
-//   k_count    -> per-chunk left counts (ballot+popc) + per-node totals
-//   k_check    -> degenerate spatial splits fall back to object median
-//   radix      -> (object nodes only) 12 x 8-bit MSD radix select of the (x_c, id) median
-//   scan       -> CUB exclusive scan of the chunk left counts
-//   k_children -> child node records in left-to-right (BFS) order
-//   k_scatter  -> stable partition into the ping-pong buffer; finished leaves written in place
-// then k_veb (per level, top-down) computes each node's vEB slot and k_emit writes
-// the canonical node array and the traversal nodes (TNode) in vEB order.
-#include <cub/cub.cuh>
+// k_build<D> (cooperative, grid = co-resident blocks, sized to n) runs, for
+// every level L (all nodes of the level at once):
+//   A  per node:  chunk counts (<=1024-point chunks), bbox accumulators reset
+//   -  grid scan: chunk offsets
+//   B  per chunk (one warp): chunk->node, coalesced fp64 loads, warp min/max, one atomic per chunk
+//   C  per node:  node record, leaf / spatial split / object flag
+//   D  per chunk: left counts (ballot + popc) + per-node totals
+//   E  per node:  degenerate spatial splits -> object median; internal flags
+//   O  (object nodes only) 12 x 8-bit MSD radix select of the (x_c, id) median
+//   -  grid scans: internal ranks (BFS child slots) and chunk left-count offsets
+//   F  per node:  child records in left-to-right (BFS) order
+//   G  per chunk: stable partition into the ping-pong buffer; finished leaves written in place
+// then, per depth top-down, each node's vEB slot (cut frame of its depth,
+// range propagation over the level arrays).  A second small kernel (after the
+// host learns the exact node count) writes the canonical nodes and the
+// traversal nodes (TNode) in vEB order.
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <vector>
 
 #include "gk_common.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace gk {
 namespace {
 
 constexpr std::uint8_t F_LEAF = 1, F_OBJECT = 2;
+constexpr int kThreads = 256;
+constexpr int kSelCap = 4096;  // object nodes per radix-select batch
+constexpr int kMaxLevels = 256;
 
 __host__ __device__ inline std::uint64_t hyperceiling_u(std::uint64_t x) {
   std::uint64_t p = 1;
@@ -46,387 +57,498 @@ struct NodeArrays {
   double *split, *lo, *hi;
 };
 
-// ------------------------------------------------------------------ chunks --
-__global__ void k_chunk_counts(const std::uint32_t* __restrict__ count, std::uint32_t S, std::uint32_t* out) {
-  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < S) out[v] = (count[v] + kChunk - 1) / kChunk;
-  else if (v == S) out[v] = 0;
-}
-
-__global__ void k_chunk_node(const std::uint32_t* __restrict__ chunk_off, std::uint32_t S, std::uint32_t* chunk_node) {
-  const std::uint32_t total = chunk_off[S];
-  for (std::uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
-    std::uint32_t lo = 0, hi = S;  // largest v with chunk_off[v] <= c
-    while (hi - lo > 1) {
-      std::uint32_t mid = (lo + hi) >> 1;
-      if (chunk_off[mid] <= c) lo = mid; else hi = mid;
-    }
-    chunk_node[c] = lo;
-  }
-}
-
-struct ChunkIt {
-  std::uint32_t v, first, len;
-};
-__device__ __forceinline__ ChunkIt chunk_at(std::uint32_t c, const std::uint32_t* chunk_off, const std::uint32_t* chunk_node,
-                                            const std::uint32_t* start, const std::uint32_t* count, std::uint32_t off) {
-  ChunkIt it;
-  it.v = chunk_node[c];
-  std::uint32_t g = off + it.v;
-  std::uint32_t s = start[g], n = count[g];
-  it.first = s + (c - chunk_off[it.v]) * kChunk;
-  it.len = min(static_cast<std::uint32_t>(kChunk), s + n - it.first);
-  return it;
-}
-
-// -------------------------------------------------------------------- bbox --
-__global__ void k_bbox_init(unsigned long long* keys, std::uint32_t n_keys_half) {
-  std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_keys_half) { keys[2 * i] = ~0ULL; keys[2 * i + 1] = 0ULL; }
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) k_bbox(const double* __restrict__ cur, std::uint64_t stride,
-                                              const std::uint32_t* __restrict__ chunk_off,
-                                              const std::uint32_t* __restrict__ chunk_node, std::uint32_t S,
-                                              std::uint32_t off, NodeArrays na, unsigned long long* keys) {
-  const std::uint32_t total = chunk_off[S];
-  const int lane = threadIdx.x & 31;
-  const std::uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (std::uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < total; c += nw) {
-    ChunkIt it = chunk_at(c, chunk_off, chunk_node, na.start, na.count, off);
-    double lo[D], hi[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) { lo[j] = __longlong_as_double(0x7ff0000000000000LL); hi[j] = -lo[j]; }
-    for (std::uint32_t i = it.first + lane; i < it.first + it.len; i += 32) {
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        double x = cur[j * stride + i];
-        lo[j] = fmin(lo[j], x);
-        hi[j] = fmax(hi[j], x);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo[j] = fmin(lo[j], __shfl_xor_sync(0xffffffffu, lo[j], o));
-        hi[j] = fmax(hi[j], __shfl_xor_sync(0xffffffffu, hi[j], o));
-      }
-    }
-    if (lane < D) {
-      double l = lo[0], h = hi[0];
-#pragma unroll
-      for (int j = 1; j < D; ++j)
-        if (lane == j) { l = lo[j]; h = hi[j]; }
-      unsigned long long* kk = keys + (static_cast<std::uint64_t>(it.v) * D + lane) * 2;
-      atomicMin(kk, dkey(l));
-      atomicMax(kk + 1, dkey(h));
-    }
-  }
-}
-
-// ------------------------------------------------------------------- split --
-template <int D>
-__global__ void k_split(std::uint32_t S, std::uint32_t off, int level, int leaf, int heuristic,
-                        const unsigned long long* __restrict__ keys, NodeArrays na) {
-  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= S) return;
-  const std::uint32_t g = off + v;
-  double lo[D], hi[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    lo[j] = dkey_inv(keys[(static_cast<std::uint64_t>(v) * D + j) * 2]);
-    hi[j] = dkey_inv(keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1]);
-    na.lo[static_cast<std::uint64_t>(g) * D + j] = lo[j];
-    na.hi[static_cast<std::uint64_t>(g) * D + j] = hi[j];
-  }
-  na.nleft[g] = 0;
-  na.level[g] = static_cast<std::uint8_t>(level);
-  if (na.count[g] <= static_cast<std::uint32_t>(leaf)) {
-    na.flags[g] = F_LEAF;
-    na.split[g] = 0.0;
-    return;
-  }
-  const int c = level % D;
-  if (heuristic == GK_OBJECT_MEDIAN || level >= kDepthCap) {
-    na.flags[g] = F_OBJECT;
-    na.split[g] = 0.0;
-  } else {
-    na.flags[g] = 0;
-    double l = lo[0], h = hi[0];
-#pragma unroll
-    for (int j = 1; j < D; ++j)
-      if (c == j) { l = lo[j]; h = hi[j]; }
-    na.split[g] = __dmul_rn(__dadd_rn(l, h), 0.5);  // (lo + hi) / 2 exactly
-  }
-}
-
-// ------------------------------------------------------------------- count --
-// pass 0: spatial nodes (x_c < s); pass 1: object nodes ((x_c, id) < threshold)
-template <int D>
-__global__ void __launch_bounds__(256) k_count(const double* __restrict__ cur, const std::uint32_t* __restrict__ cur_ids,
-                                               std::uint64_t stride, const std::uint32_t* __restrict__ chunk_off,
-                                               const std::uint32_t* __restrict__ chunk_node, std::uint32_t S,
-                                               std::uint32_t off, int level, int pass, NodeArrays na,
-                                               std::uint32_t* chunk_left) {
-  const std::uint32_t total = chunk_off[S];
-  const int lane = threadIdx.x & 31;
-  const std::uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const int cdim = level % D;
-  for (std::uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < total; c += nw) {
-    ChunkIt it = chunk_at(c, chunk_off, chunk_node, na.start, na.count, off);
-    const std::uint32_t g = off + it.v;
-    const std::uint8_t fl = na.flags[g];
-    if (fl & F_LEAF) { if (pass == 0 && lane == 0) chunk_left[c] = 0; continue; }
-    const bool obj = (fl & F_OBJECT) != 0;
-    if (pass == 0 && obj) { if (lane == 0) chunk_left[c] = 0; continue; }
-    if (pass == 1 && !obj) continue;
-    const double s = na.split[g];
-    const std::uint32_t tid = na.thr_id[g];
-    const double* xc = cur + cdim * stride;
-    std::uint32_t cnt = 0;
-    for (std::uint32_t i0 = it.first; i0 < it.first + it.len; i0 += 32) {
-      const std::uint32_t i = i0 + lane;
-      bool p = false;
-      if (i < it.first + it.len) {
-        double x = xc[i];
-        p = obj ? (x < s || (x == s && cur_ids[i] < tid)) : (x < s);
-      }
-      cnt += __popc(__ballot_sync(0xffffffffu, p));
-    }
-    if (lane == 0) {
-      chunk_left[c] = cnt;
-      if (pass == 0) atomicAdd(&na.nleft[g], cnt);
-    }
-  }
-}
-
-// degenerate spatial splits -> object median; internal flags for the BFS scan
-__global__ void k_check(std::uint32_t S, std::uint32_t off, NodeArrays na, std::uint32_t* is_int,
-                        std::uint32_t* obj_list, std::uint32_t* counters) {
-  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v == S) is_int[S] = 0;
-  if (v >= S) return;
-  const std::uint32_t g = off + v;
-  std::uint8_t fl = na.flags[g];
-  if (fl & F_LEAF) { is_int[v] = 0; return; }
-  is_int[v] = 1;
-  if (!(fl & F_OBJECT)) {
-    std::uint32_t nl = na.nleft[g];
-    if (nl == 0 || nl == na.count[g]) { fl |= F_OBJECT; na.flags[g] = fl; }
-  }
-  if (fl & F_OBJECT) {
-    std::uint32_t o = atomicAdd(&counters[0], 1u);
-    obj_list[o] = g;
-    na.nleft[g] = na.count[g] / 2;
-    na.pos[g] = o;  // temporary: object index (pos is recomputed by k_veb)
-  }
-}
-
-// ------------------------------------------------------- object median select --
 struct SelState {
   unsigned long long hi;  // known high digits of dkey(x_c)
   std::uint32_t lo;       // known digits of the id
   std::uint32_t rank;     // rank still to skip inside the current prefix bucket
 };
 
-__global__ void k_sel_init(std::uint32_t nobj, const std::uint32_t* obj_list, NodeArrays na, SelState* st) {
-  std::uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= nobj) return;
-  st[o].hi = 0; st[o].lo = 0; st[o].rank = na.count[obj_list[o]] / 2;
+// control words (device)
+enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_COUNT = 8 };
+
+struct BuildArgs {
+  int leaf, heuristic;
+  std::uint32_t n;
+  const double* src;
+  std::uint64_t src_stride;
+  const std::uint32_t* src_ids;
+  double *bufA, *bufB;
+  std::uint32_t *idsA, *idsB;
+  double* out;
+  std::uint32_t* out_ids;
+  NodeArrays na;
+  std::uint32_t* lvl_off;   // [kMaxLevels + 2]
+  std::uint32_t* ctrl;      // [C_COUNT]
+  std::uint32_t *chunk_cnt, *chunk_off, *chunk_node, *chunk_left, *left_scan, *is_int, *irank, *obj_list;
+  unsigned long long* keys;
+  SelState* sel;
+  std::uint32_t* hist;      // [kSelCap * 256]
+  std::uint32_t* bsum;      // [gridDim]
+  std::uint32_t* int_by_slot;  // [cap + 1]
+};
+
+// ------------------------------------------------------------ block helpers --
+__device__ __forceinline__ std::uint32_t block_sum(std::uint32_t v, std::uint32_t* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  std::uint32_t t = 0;
+  for (int i = 0; i < (kThreads >> 5); ++i) t += sh[i];
+  return t;
 }
 
-// digit p in 0..11: p < 8 -> byte (7-p) of the 64-bit key, else byte (11-p) of the id
-template <int D>
-__global__ void __launch_bounds__(256) k_sel_hist(const double* __restrict__ cur, const std::uint32_t* __restrict__ cur_ids,
-                                                  std::uint64_t stride, const std::uint32_t* __restrict__ chunk_off,
-                                                  const std::uint32_t* __restrict__ chunk_node, std::uint32_t S,
-                                                  std::uint32_t off, int level, int p, NodeArrays na,
-                                                  const SelState* __restrict__ st, std::uint32_t* hist) {
-  const std::uint32_t total = chunk_off[S];
-  const int lane = threadIdx.x & 31;
-  const std::uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const int cdim = level % D;
-  for (std::uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < total; c += nw) {
-    ChunkIt it = chunk_at(c, chunk_off, chunk_node, na.start, na.count, off);
-    const std::uint32_t g = off + it.v;
-    if ((na.flags[g] & (F_LEAF | F_OBJECT)) != F_OBJECT) continue;
-    const std::uint32_t o = na.pos[g];
-    const SelState s = st[o];
-    for (std::uint32_t i0 = it.first; i0 < it.first + it.len; i0 += 32) {
-      const std::uint32_t i = i0 + lane;
-      int digit = -1;
-      if (i < it.first + it.len) {
-        unsigned long long k = dkey(__dadd_rn(cur[cdim * stride + i], 0.0));  // -0 == +0 as in the oracle
-        std::uint32_t id = cur_ids[i];
-        bool match;
-        if (p < 8) {
-          const int sh = 8 * (8 - p);  // bits above the current digit
-          match = (sh >= 64) ? true : ((k >> sh) == (s.hi >> sh));
-          digit = static_cast<int>((k >> (8 * (7 - p))) & 0xff);
-        } else {
-          const int q = p - 8;
-          const int sh = 8 * (4 - q);
-          match = (k == s.hi) && ((sh >= 32) ? true : ((id >> sh) == (s.lo >> sh)));
-          digit = static_cast<int>((id >> (8 * (3 - q))) & 0xff);
-        }
-        if (!match) digit = -1;
-      }
-      unsigned peers = __match_any_sync(0xffffffffu, digit);
-      int leader = __ffs(peers) - 1;
-      if (digit >= 0 && lane == leader) atomicAdd(&hist[o * 256 + digit], __popc(peers));
+__device__ __forceinline__ void sync_all(cg::grid_group& grid) {
+  grid.sync();
+  __threadfence();  // gpu-scope fence: also invalidates this SM's L1 (CCTL.IVALL)
+}
+
+// exclusive scan of in[0, n) into out, all blocks of the grid (one grid barrier inside)
+__device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::uint32_t* out, std::uint32_t n,
+                          std::uint32_t* bsum, std::uint32_t* sh) {
+  const std::uint32_t G = gridDim.x, b = blockIdx.x;
+  const std::uint32_t seg = (n + G - 1) / G;
+  const std::uint32_t lo = min(n, b * seg), hi = min(n, lo + seg);
+  std::uint32_t s = 0;
+  for (std::uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += __ldcg(&in[i]);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) bsum[b] = s;
+  sync_all(grid);
+  std::uint32_t o = 0;
+  for (std::uint32_t i = threadIdx.x; i < b; i += blockDim.x) o += __ldcg(&bsum[i]);
+  o = block_sum(o, sh);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  std::uint32_t carry = o;
+  for (std::uint32_t base = lo; base < hi; base += blockDim.x) {
+    const std::uint32_t i = base + threadIdx.x;
+    const std::uint32_t v = i < hi ? __ldcg(&in[i]) : 0u;
+    std::uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
     }
+    __syncthreads();
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    std::uint32_t wpre = 0, tot = 0;
+    for (int j = 0; j < (kThreads >> 5); ++j) {
+      const std::uint32_t t = sh[j];
+      if (j < w) wpre += t;
+      tot += t;
+    }
+    if (i < hi) out[i] = carry + wpre + x - v;
+    carry += tot;
   }
 }
 
-__global__ void k_sel_pick(std::uint32_t nobj, int p, SelState* st, std::uint32_t* hist) {
-  std::uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= nobj) return;
-  SelState s = st[o];
-  std::uint32_t* h = hist + o * 256;
-  std::uint32_t acc = 0;
-  int dsel = 255;
-  for (int dgt = 0; dgt < 256; ++dgt) {
-    std::uint32_t c = h[dgt];
-    if (s.rank < acc + c) { dsel = dgt; break; }
-    acc += c;
-  }
-  s.rank -= acc;
-  if (p < 8) s.hi |= static_cast<unsigned long long>(dsel) << (8 * (7 - p));
-  else s.lo |= static_cast<std::uint32_t>(dsel) << (8 * (3 - (p - 8)));
-  st[o] = s;
-  for (int dgt = 0; dgt < 256; ++dgt) h[dgt] = 0;
-}
-
-__global__ void k_sel_finish(std::uint32_t nobj, const std::uint32_t* obj_list, const SelState* st, NodeArrays na) {
-  std::uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= nobj) return;
-  const std::uint32_t g = obj_list[o];
-  na.split[g] = dkey_inv(st[o].hi);  // canonical +0 for a zero median
-  na.thr_id[g] = st[o].lo;
-}
-
-// ---------------------------------------------------------------- children --
-__global__ void k_children(std::uint32_t S, std::uint32_t off, std::uint32_t next_off, const std::uint32_t* __restrict__ irank,
-                           NodeArrays na) {
-  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= S) return;
-  const std::uint32_t g = off + v;
-  const std::uint32_t cb = next_off + 2 * irank[v];
-  na.cbase[g] = cb;
-  if (na.flags[g] & F_LEAF) return;
-  const std::uint32_t s = na.start[g], n = na.count[g], nl = na.nleft[g];
-  na.start[cb] = s; na.count[cb] = nl; na.parent[cb] = g;
-  na.start[cb + 1] = s + nl; na.count[cb + 1] = n - nl; na.parent[cb + 1] = g;
-}
-
-// ----------------------------------------------------------------- scatter --
+// -------------------------------------------------------------- the build --
 template <int D>
-__global__ void __launch_bounds__(256) k_scatter(const double* __restrict__ cur, const std::uint32_t* __restrict__ cur_ids,
-                                                 std::uint64_t stride, double* __restrict__ nxt,
-                                                 std::uint32_t* __restrict__ nxt_ids, double* __restrict__ out,
-                                                 std::uint32_t* __restrict__ out_ids, std::uint64_t n,
-                                                 const std::uint32_t* __restrict__ chunk_off,
-                                                 const std::uint32_t* __restrict__ chunk_node,
-                                                 const std::uint32_t* __restrict__ left_scan, std::uint32_t S,
-                                                 std::uint32_t off, int level, NodeArrays na) {
-  const std::uint32_t total = chunk_off[S];
+__global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ std::uint32_t sh[32];
+  const NodeArrays& na = a.na;
+  const std::uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const std::uint32_t gthreads = gridDim.x * blockDim.x;
+  const std::uint32_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const std::uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const int cdim = level % D;
-  for (std::uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < total; c += nw) {
-    ChunkIt it = chunk_at(c, chunk_off, chunk_node, na.start, na.count, off);
-    const std::uint32_t g = off + it.v;
-    const std::uint8_t fl = na.flags[g];
-    const std::uint32_t end = it.first + it.len;
-    if (fl & F_LEAF) {  // finished: positions are final
-      for (std::uint32_t i = it.first + lane; i < end; i += 32) {
+  const std::uint32_t n = a.n;
+
+  const double* cur = a.src;
+  const std::uint32_t* cur_ids = a.src_ids;
+  std::uint64_t cur_stride = a.src_stride;
+  double* nxt = a.bufA;
+  std::uint32_t* nxt_ids = a.idsA;
+
+  if (gtid == 0) {
+    na.start[0] = 0; na.count[0] = n; na.parent[0] = 0xffffffffu;
+    a.lvl_off[0] = 0;
+    a.ctrl[C_S] = 1;
+  }
+  sync_all(grid);
+
+  int level = 0;
+  for (;; ++level) {
+    const std::uint32_t S = __ldcg(&a.ctrl[C_S]);
+    if (S == 0 || level >= kMaxLevels) break;
+    const std::uint32_t off = __ldcg(&a.lvl_off[level]);
+    const int cdim = level % D;
+
+    // A: chunk counts, bbox accumulator reset
+    for (std::uint32_t v = gtid; v <= S; v += gthreads) {
+      if (v < S) {
+        a.chunk_cnt[v] = (__ldcg(&na.count[off + v]) + kChunk - 1) / kChunk;
 #pragma unroll
-        for (int j = 0; j < D; ++j) out[j * n + i] = cur[j * stride + i];
-        out_ids[i] = cur_ids[i];
+        for (int j = 0; j < D; ++j) {
+          a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2] = ~0ULL;
+          a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1] = 0ULL;
+        }
+        na.nleft[off + v] = 0;
+      } else {
+        a.chunk_cnt[S] = 0;
       }
-      continue;
     }
-    const bool obj = (fl & F_OBJECT) != 0;
-    const double s = na.split[g];
-    const std::uint32_t tid = na.thr_id[g];
-    const std::uint32_t nstart = na.start[g], nl = na.nleft[g];
-    std::uint32_t lbefore = left_scan[c] - left_scan[chunk_off[it.v]];
-    for (std::uint32_t i0 = it.first; i0 < end; i0 += 32) {
-      const std::uint32_t i = i0 + lane;
-      bool valid = i < end;
-      bool p = false;
-      double x[D];
-      std::uint32_t id = 0;
-      if (valid) {
+    if (gtid == 0) a.ctrl[C_NOBJ] = 0;
+    sync_all(grid);
+    grid_scan(grid, a.chunk_cnt, a.chunk_off, S + 1, a.bsum, sh);
+    sync_all(grid);
+    const std::uint32_t nchunks = __ldcg(&a.chunk_off[S]);
+
+    // B: per chunk: owning node (binary search) + bounding box
+    for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
+      std::uint32_t lo = 0, hi = S;
+      while (hi - lo > 1) {
+        const std::uint32_t mid = (lo + hi) >> 1;
+        if (__ldcg(&a.chunk_off[mid]) <= c) lo = mid; else hi = mid;
+      }
+      const std::uint32_t v = lo, g = off + v;
+      if (lane == 0) a.chunk_node[c] = v;
+      const std::uint32_t s0 = __ldcg(&na.start[g]), cnt = __ldcg(&na.count[g]);
+      const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
+      const std::uint32_t end = min(first + kChunk, s0 + cnt);
+      double mn[D], mx[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) x[j] = cur[j * stride + i];
-        id = cur_ids[i];
-        double xc = x[0];
+      for (int j = 0; j < D; ++j) { mn[j] = __longlong_as_double(0x7ff0000000000000LL); mx[j] = -mn[j]; }
+      for (std::uint32_t i = first + lane; i < end; i += 32) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double x = __ldcg(&cur[j * cur_stride + i]);
+          mn[j] = fmin(mn[j], x);
+          mx[j] = fmax(mx[j], x);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mn[j] = fmin(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
+          mx[j] = fmax(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
+        }
+      }
+      if (lane < D) {
+        double l = mn[0], h = mx[0];
 #pragma unroll
         for (int j = 1; j < D; ++j)
-          if (cdim == j) xc = x[j];
-        p = obj ? (xc < s || (xc == s && id < tid)) : (xc < s);
+          if (lane == j) { l = mn[j]; h = mx[j]; }
+        unsigned long long* kk = a.keys + (static_cast<std::uint64_t>(v) * D + lane) * 2;
+        atomicMin(kk, dkey(l));
+        atomicMax(kk + 1, dkey(h));
       }
-      unsigned b = __ballot_sync(0xffffffffu, p);
-      if (valid) {
-        std::uint32_t lrank = lbefore + __popc(b & lt_mask);
-        std::uint32_t np = p ? nstart + lrank : nstart + nl + (i - nstart - lrank);
+    }
+    sync_all(grid);
+
+    // C: node records and split decisions
+    for (std::uint32_t v = gtid; v < S; v += gthreads) {
+      const std::uint32_t g = off + v;
+      double lo[D], hi[D];
 #pragma unroll
-        for (int j = 0; j < D; ++j) nxt[j * n + np] = x[j];
-        nxt_ids[np] = id;
+      for (int j = 0; j < D; ++j) {
+        lo[j] = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2]));
+        hi[j] = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1]));
+        na.lo[static_cast<std::uint64_t>(g) * D + j] = lo[j];
+        na.hi[static_cast<std::uint64_t>(g) * D + j] = hi[j];
       }
-      lbefore += __popc(b);
+      na.level[g] = static_cast<std::uint8_t>(level);
+      if (__ldcg(&na.count[g]) <= static_cast<std::uint32_t>(a.leaf)) {
+        na.flags[g] = F_LEAF;
+        na.split[g] = 0.0;
+      } else if (a.heuristic == GK_OBJECT_MEDIAN || level >= kDepthCap) {
+        na.flags[g] = F_OBJECT;
+        na.split[g] = 0.0;
+      } else {
+        na.flags[g] = 0;
+        double l = lo[0], h = hi[0];
+#pragma unroll
+        for (int j = 1; j < D; ++j)
+          if (cdim == j) { l = lo[j]; h = hi[j]; }
+        na.split[g] = __dmul_rn(__dadd_rn(l, h), 0.5);  // (lo + hi) / 2 exactly
+      }
     }
-  }
-}
+    sync_all(grid);
 
-// -------------------------------------------------------------------- vEB --
-__device__ __forceinline__ std::uint32_t child_idx(std::uint32_t x, int e, const std::uint32_t* lvl_off,
-                                                   const std::uint32_t* cbase) {
-  return (x < lvl_off[e + 1]) ? cbase[x] : lvl_off[e + 2];
-}
-
-// vEB slot of every node at depth d: d is the cut depth of frame (d0, l) whose
-// root r is d's ancestor at depth d0; pos = pos(r) + |top part| + sizes of the
-// bottom subtrees left of v's (all sizes restricted to the frame's levels).
-__global__ void k_veb(int d, int d0, int l, const std::uint32_t* __restrict__ lvl_off, NodeArrays na) {
-  const std::uint32_t off = lvl_off[d];
-  const std::uint32_t S = lvl_off[d + 1] - off;
-  std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= S) return;
-  const std::uint32_t g = off + v;
-  std::uint32_t r = g;
-  for (int e = d; e > d0; --e) r = na.parent[r];
-  std::uint32_t lo = r, hi = r + 1, top = 0;
-  for (int e = d0; e < d; ++e) {
-    top += hi - lo;
-    lo = child_idx(lo, e, lvl_off, na.cbase);
-    hi = child_idx(hi, e, lvl_off, na.cbase);
-  }
-  std::uint32_t a = g, b = lo, left = 0;
-  for (int e = d; e < d0 + l; ++e) {
-    left += a - b;
-    if (e + 1 < d0 + l) {
-      a = child_idx(a, e, lvl_off, na.cbase);
-      b = child_idx(b, e, lvl_off, na.cbase);
+    // D: spatial left counts per chunk (x_c < s)
+    for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
+      const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+      const std::uint8_t fl = __ldcg(&na.flags[g]);
+      std::uint32_t cnt = 0;
+      if (!(fl & (F_LEAF | F_OBJECT))) {
+        const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
+        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
+        const std::uint32_t end = min(first + kChunk, s0 + nn);
+        const double s = __ldcg(&na.split[g]);
+        const double* xc = cur + cdim * cur_stride;
+        for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
+          const std::uint32_t i = i0 + lane;
+          cnt += __popc(__ballot_sync(0xffffffffu, i < end && __ldcg(&xc[i]) < s));
+        }
+        if (lane == 0 && cnt) atomicAdd(&na.nleft[g], cnt);
+      }
+      if (lane == 0) a.chunk_left[c] = cnt;
     }
+    if (gtid == 0) a.chunk_left[nchunks] = 0;
+    sync_all(grid);
+
+    // E: degenerate spatial splits -> object median; internal flags
+    for (std::uint32_t v = gtid; v <= S; v += gthreads) {
+      if (v == S) { a.is_int[S] = 0; continue; }
+      const std::uint32_t g = off + v;
+      std::uint8_t fl = __ldcg(&na.flags[g]);
+      if (fl & F_LEAF) { a.is_int[v] = 0; continue; }
+      a.is_int[v] = 1;
+      const std::uint32_t cnt = __ldcg(&na.count[g]);
+      if (!(fl & F_OBJECT)) {
+        const std::uint32_t nl = __ldcg(&na.nleft[g]);
+        if (nl == 0 || nl == cnt) { fl |= F_OBJECT; na.flags[g] = fl; }
+      }
+      if (fl & F_OBJECT) {
+        const std::uint32_t o = atomicAdd(&a.ctrl[C_NOBJ], 1u);
+        a.obj_list[o] = g;
+        na.nleft[g] = cnt / 2;
+        na.pos[g] = o;  // temporary: object index (pos is recomputed by the vEB phase)
+      }
+    }
+    sync_all(grid);
+
+    // O: object-median radix select (batches of kSelCap object nodes)
+    const std::uint32_t nobj = __ldcg(&a.ctrl[C_NOBJ]);
+    for (std::uint32_t b0 = 0; b0 < nobj; b0 += kSelCap) {
+      const std::uint32_t nb = min(static_cast<std::uint32_t>(kSelCap), nobj - b0);
+      for (std::uint32_t o = gtid; o < nb * 256; o += gthreads) a.hist[o] = 0;
+      for (std::uint32_t o = gtid; o < nb; o += gthreads) {
+        a.sel[o].hi = 0;
+        a.sel[o].lo = 0;
+        a.sel[o].rank = __ldcg(&na.count[__ldcg(&a.obj_list[b0 + o])]) / 2;
+      }
+      sync_all(grid);
+      for (int p = 0; p < 12; ++p) {
+        for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
+          const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+          if ((__ldcg(&na.flags[g]) & (F_LEAF | F_OBJECT)) != F_OBJECT) continue;
+          const std::uint32_t o = __ldcg(&na.pos[g]);
+          if (o < b0 || o >= b0 + nb) continue;
+          SelState s;
+          s.hi = __ldcg(&a.sel[o - b0].hi);
+          s.lo = __ldcg(&a.sel[o - b0].lo);
+          const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
+          const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
+          const std::uint32_t end = min(first + kChunk, s0 + nn);
+          for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
+            const std::uint32_t i = i0 + lane;
+            int digit = -1;
+            if (i < end) {
+              const unsigned long long k = dkey(__dadd_rn(__ldcg(&cur[cdim * cur_stride + i]), 0.0));  // -0 == +0
+              const std::uint32_t id = __ldcg(&cur_ids[i]);
+              bool match;
+              if (p < 8) {
+                const int sh8 = 8 * (8 - p);
+                match = (sh8 >= 64) ? true : ((k >> sh8) == (s.hi >> sh8));
+                digit = static_cast<int>((k >> (8 * (7 - p))) & 0xff);
+              } else {
+                const int q = p - 8, sh8 = 8 * (4 - q);
+                match = (k == s.hi) && ((sh8 >= 32) ? true : ((id >> sh8) == (s.lo >> sh8)));
+                digit = static_cast<int>((id >> (8 * (3 - q))) & 0xff);
+              }
+              if (!match) digit = -1;
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, digit);
+            if (digit >= 0 && lane == __ffs(peers) - 1) atomicAdd(&a.hist[(o - b0) * 256 + digit], __popc(peers));
+          }
+        }
+        sync_all(grid);
+        for (std::uint32_t o = gtid; o < nb; o += gthreads) {
+          SelState s = a.sel[o];
+          std::uint32_t* h = a.hist + o * 256;
+          std::uint32_t acc = 0;
+          int dsel = 255;
+          for (int dg = 0; dg < 256; ++dg) {
+            const std::uint32_t c = __ldcg(&h[dg]);
+            if (s.rank < acc + c) { dsel = dg; break; }
+            acc += c;
+          }
+          s.rank -= acc;
+          if (p < 8) s.hi |= static_cast<unsigned long long>(dsel) << (8 * (7 - p));
+          else s.lo |= static_cast<std::uint32_t>(dsel) << (8 * (3 - (p - 8)));
+          a.sel[o] = s;
+          for (int dg = 0; dg < 256; ++dg) h[dg] = 0;
+          if (p == 11) {
+            const std::uint32_t g = __ldcg(&a.obj_list[b0 + o]);
+            na.split[g] = dkey_inv(s.hi);  // canonical +0 for a zero median
+            na.thr_id[g] = s.lo;
+          }
+        }
+        sync_all(grid);
+      }
+    }
+    if (nobj) {  // left counts of object nodes ((x_c, id) < threshold)
+      for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
+        const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+        if ((__ldcg(&na.flags[g]) & (F_LEAF | F_OBJECT)) != F_OBJECT) continue;
+        const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
+        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
+        const std::uint32_t end = min(first + kChunk, s0 + nn);
+        const double s = __ldcg(&na.split[g]);
+        const std::uint32_t tid = __ldcg(&na.thr_id[g]);
+        std::uint32_t cnt = 0;
+        for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
+          const std::uint32_t i = i0 + lane;
+          bool pr = false;
+          if (i < end) {
+            const double x = __ldcg(&cur[cdim * cur_stride + i]);
+            pr = x < s || (x == s && __ldcg(&cur_ids[i]) < tid);
+          }
+          cnt += __popc(__ballot_sync(0xffffffffu, pr));
+        }
+        if (lane == 0) a.chunk_left[c] = cnt;
+      }
+      sync_all(grid);
+    }
+
+    // scans: BFS child slots (internal ranks) and chunk left-count offsets
+    grid_scan(grid, a.is_int, a.irank, S + 1, a.bsum, sh);
+    sync_all(grid);
+    grid_scan(grid, a.chunk_left, a.left_scan, nchunks + 1, a.bsum, sh);
+    sync_all(grid);
+    const std::uint32_t nint = __ldcg(&a.irank[S]);
+    const std::uint32_t next_off = off + S;
+
+    // F: child node records; G: stable partition
+    for (std::uint32_t v = gtid; v < S; v += gthreads) {
+      const std::uint32_t g = off + v;
+      const std::uint32_t cb = next_off + 2 * __ldcg(&a.irank[v]);
+      na.cbase[g] = cb;
+      if (__ldcg(&na.flags[g]) & F_LEAF) continue;
+      const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]), nl = __ldcg(&na.nleft[g]);
+      na.start[cb] = s0; na.count[cb] = nl; na.parent[cb] = g;
+      na.start[cb + 1] = s0 + nl; na.count[cb + 1] = nn - nl; na.parent[cb + 1] = g;
+    }
+    for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
+      const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+      const std::uint8_t fl = __ldcg(&na.flags[g]);
+      const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
+      const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
+      const std::uint32_t end = min(first + kChunk, s0 + nn);
+      if (fl & F_LEAF) {  // finished: positions are final
+        for (std::uint32_t i = first + lane; i < end; i += 32) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) a.out[j * static_cast<std::uint64_t>(n) + i] = __ldcg(&cur[j * cur_stride + i]);
+          a.out_ids[i] = __ldcg(&cur_ids[i]);
+        }
+        continue;
+      }
+      const bool obj = (fl & F_OBJECT) != 0;
+      const double s = __ldcg(&na.split[g]);
+      const std::uint32_t tid = obj ? __ldcg(&na.thr_id[g]) : 0u;
+      const std::uint32_t nl = __ldcg(&na.nleft[g]);
+      std::uint32_t lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&a.chunk_off[v])]);
+      for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
+        const std::uint32_t i = i0 + lane;
+        const bool valid = i < end;
+        bool pr = false;
+        double x[D];
+        std::uint32_t id = 0;
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) x[j] = __ldcg(&cur[j * cur_stride + i]);
+          id = __ldcg(&cur_ids[i]);
+          double xc = x[0];
+#pragma unroll
+          for (int j = 1; j < D; ++j)
+            if (cdim == j) xc = x[j];
+          pr = obj ? (xc < s || (xc == s && id < tid)) : (xc < s);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, pr);
+        if (valid) {
+          const std::uint32_t lrank = lbefore + __popc(bal & lt_mask);
+          const std::uint32_t np = pr ? s0 + lrank : s0 + nl + (i - s0 - lrank);
+#pragma unroll
+          for (int j = 0; j < D; ++j) nxt[j * static_cast<std::uint64_t>(n) + np] = x[j];
+          nxt_ids[np] = id;
+        }
+        lbefore += __popc(bal);
+      }
+    }
+    if (gtid == 0) {
+      a.lvl_off[level + 1] = next_off;
+      a.ctrl[C_S] = 2 * nint;
+    }
+    // ping-pong: the partitioned points now live in nxt (stride n)
+    cur = nxt;
+    cur_ids = nxt_ids;
+    cur_stride = n;
+    nxt = (nxt == a.bufA) ? a.bufB : a.bufA;
+    nxt_ids = (nxt_ids == a.idsA) ? a.idsB : a.idsA;
+    sync_all(grid);
   }
-  na.pos[g] = na.pos[r] + top + left;
+
+  // ---- vEB slots, top-down.  Depth d is the cut depth of exactly one frame
+  // (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
+  // pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees
+  // left of v's, all restricted to the frame's levels (range propagation).
+  const int H = level;
+  const std::uint32_t N = __ldcg(&a.lvl_off[H]);
+  if (gtid == 0) {
+    a.lvl_off[H + 1] = N;
+    a.ctrl[C_H] = static_cast<std::uint32_t>(H);
+    a.ctrl[C_N] = N;
+    na.pos[0] = 0;
+  }
+  sync_all(grid);
+  for (int d = 1; d < H; ++d) {
+    int d0 = 0, l = H;  // locate the frame whose cut is at depth d
+    while (true) {
+      const int lb = static_cast<int>(hyperceiling_u(static_cast<std::uint64_t>((l + 1) / 2)));
+      const int lt = l - lb;
+      if (d == d0 + lt) break;
+      if (d < d0 + lt) l = lt;
+      else { d0 += lt; l = lb; }
+    }
+    const std::uint32_t off = __ldcg(&a.lvl_off[d]), S = __ldcg(&a.lvl_off[d + 1]) - off;
+    for (std::uint32_t v = gtid; v < S; v += gthreads) {
+      const std::uint32_t g = off + v;
+      std::uint32_t r = g;
+      for (int e = d; e > d0; --e) r = __ldcg(&na.parent[r]);
+      auto child_idx = [&](std::uint32_t x, int e) -> std::uint32_t {
+        return (x < __ldcg(&a.lvl_off[e + 1])) ? __ldcg(&na.cbase[x]) : __ldcg(&a.lvl_off[e + 2]);
+      };
+      std::uint32_t lo = r, hi = r + 1, top = 0;
+      for (int e = d0; e < d; ++e) {
+        top += hi - lo;
+        lo = child_idx(lo, e);
+        hi = child_idx(hi, e);
+      }
+      std::uint32_t x = g, y = lo, left = 0;
+      for (int e = d; e < d0 + l; ++e) {
+        left += x - y;
+        if (e + 1 < d0 + l) {
+          x = child_idx(x, e);
+          y = child_idx(y, e);
+        }
+      }
+      na.pos[g] = __ldcg(&na.pos[r]) + top + left;
+    }
+    sync_all(grid);
+  }
+  // slot -> internal flag (scanned into internal ranks = TNode indices by k_slot_rank)
+  for (std::uint32_t g = gtid; g <= N; g += gthreads) {
+    if (g == N) a.int_by_slot[N] = 0;
+    else a.int_by_slot[__ldcg(&na.pos[g])] = (__ldcg(&na.flags[g]) & F_LEAF) ? 0u : 1u;
+  }
 }
 
-__global__ void k_slot_flags(std::uint32_t N, NodeArrays na, std::uint32_t* int_by_slot) {
-  std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g == N) int_by_slot[N] = 0;
-  if (g >= N) return;
-  int_by_slot[na.pos[g]] = (na.flags[g] & F_LEAF) ? 0u : 1u;
+__global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::uint32_t* irank_by_slot) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ std::uint32_t sh[32];
+  const std::uint32_t N = __ldcg(&a.ctrl[C_N]);
+  grid_scan(grid, a.int_by_slot, irank_by_slot, N + 1, a.bsum, sh);
 }
 
 template <int D>
-__global__ void k_emit(std::uint32_t N, NodeArrays na, const std::uint32_t* __restrict__ irank_by_slot,
+__global__ void k_emit(const BuildArgs a, std::uint32_t N, const std::uint32_t* __restrict__ irank_by_slot,
                        gk_canon_node* canon, TNode<D>* tn, std::int32_t* orig) {
+  const NodeArrays& na = a.na;
   std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= N) return;
   const std::uint32_t slot = na.pos[g];
@@ -485,197 +607,8 @@ void dfree(T*& p, cudaStream_t st) {
   if (p) GK_CUDA(cudaFreeAsync(p, st));
   p = nullptr;
 }
-
-struct Scratch {
-  void* cub = nullptr;
-  std::size_t cub_bytes = 0;
-  cudaStream_t st;
-  explicit Scratch(cudaStream_t s) : st(s) {}
-  ~Scratch() { if (cub) cudaFreeAsync(cub, st); }
-  void scan(const std::uint32_t* in, std::uint32_t* out, std::uint64_t n) {
-    std::size_t need = 0;
-    GK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, static_cast<int>(n), st));
-    if (need > cub_bytes) {
-      if (cub) GK_CUDA(cudaFreeAsync(cub, st));
-      cub_bytes = std::max(need, cub_bytes * 2);
-      GK_CUDA(cudaMallocAsync(&cub, cub_bytes, st));
-    }
-    GK_CUDA(cub::DeviceScan::ExclusiveSum(cub, need, in, out, static_cast<int>(n), st));
-  }
-};
-
-inline unsigned blocks_for(std::uint64_t n, unsigned t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
-
-// cut frame (d0, l) for every depth 1..H-1 of the vEB recursion over H levels
-void veb_cuts(int d0, int l, std::vector<std::pair<int, int>>& cut) {
-  if (l <= 1) return;
-  int lb = static_cast<int>(hyperceiling_u(static_cast<std::uint64_t>((l + 1) / 2)));
-  int lt = l - lb;
-  cut[d0 + lt] = {d0, l};
-  veb_cuts(d0, lt, cut);
-  veb_cuts(d0 + lt, lb, cut);
-}
-
-template <int D>
-void build_tree_d(int leaf, int heuristic, const double* src, std::uint64_t src_stride, const std::uint32_t* src_ids,
-                  std::uint64_t n, DevTree& T, cudaStream_t st) {
-  T = DevTree();
-  T.d = D;
-  T.n = n;
-  T.build_size = n;
-  T.live = n;
-  if (n == 0) return;
-  if (n >= 0xffffffffULL) throw Error(GK_ERR_INVALID, "static tree larger than 2^32-2 points");
-  const std::uint64_t cap = 2 * n - 1;
-  const int grid_w = 148 * 16;  // persistent-style grid for the chunk passes (8 warps x 16 blocks per SM)
-
-  T.coords = dalloc<double>(n * D, st);
-  T.ids = dalloc<std::uint32_t>(n, st);
-  double* bufA = dalloc<double>(n * D, st);
-  double* bufB = dalloc<double>(n * D, st);
-  std::uint32_t* idsA = dalloc<std::uint32_t>(n, st);
-  std::uint32_t* idsB = dalloc<std::uint32_t>(n, st);
-
-  NodeArrays na;
-  na.start = dalloc<std::uint32_t>(cap, st);
-  na.count = dalloc<std::uint32_t>(cap, st);
-  na.parent = dalloc<std::uint32_t>(cap, st);
-  na.cbase = dalloc<std::uint32_t>(cap, st);
-  na.nleft = dalloc<std::uint32_t>(cap, st);
-  na.pos = dalloc<std::uint32_t>(cap + 1, st);
-  na.thr_id = dalloc<std::uint32_t>(cap, st);
-  na.flags = dalloc<std::uint8_t>(cap, st);
-  na.level = dalloc<std::uint8_t>(cap, st);
-  na.split = dalloc<double>(cap, st);
-  na.lo = dalloc<double>(cap * D, st);
-  na.hi = dalloc<double>(cap * D, st);
-
-  const std::uint64_t cap_level = std::min<std::uint64_t>(cap, n);  // nodes in one level <= n
-  const std::uint64_t cap_chunks = n / kChunk + cap_level + 2;
-  std::uint32_t* chunk_cnt = dalloc<std::uint32_t>(cap_level + 1, st);
-  std::uint32_t* chunk_off = dalloc<std::uint32_t>(cap_level + 1, st);
-  std::uint32_t* chunk_node = dalloc<std::uint32_t>(cap_chunks, st);
-  std::uint32_t* chunk_left = dalloc<std::uint32_t>(cap_chunks + 1, st);
-  std::uint32_t* left_scan = dalloc<std::uint32_t>(cap_chunks + 1, st);
-  std::uint32_t* is_int = dalloc<std::uint32_t>(cap_level + 1, st);
-  std::uint32_t* irank = dalloc<std::uint32_t>(cap_level + 1, st);
-  std::uint32_t* obj_list = dalloc<std::uint32_t>(cap_level, st);
-  unsigned long long* keys = dalloc<unsigned long long>(cap_level * D * 2, st);
-  std::uint32_t* counters = dalloc<std::uint32_t>(4, st);
-  std::uint32_t* h_counters = nullptr;
-  GK_CUDA(cudaMallocHost(&h_counters, 4 * sizeof(std::uint32_t)));
-  SelState* sel = nullptr;
-  std::uint32_t* hist = nullptr;
-  std::uint64_t sel_cap = 0;
-  Scratch scratch(st);
-
-  // root
-  std::uint32_t zero = 0, n32 = static_cast<std::uint32_t>(n), none = 0xffffffffu;
-  GK_CUDA(cudaMemcpyAsync(na.start, &zero, 4, cudaMemcpyHostToDevice, st));
-  GK_CUDA(cudaMemcpyAsync(na.count, &n32, 4, cudaMemcpyHostToDevice, st));
-  GK_CUDA(cudaMemcpyAsync(na.parent, &none, 4, cudaMemcpyHostToDevice, st));
-
-  std::vector<std::uint32_t> lvl_off{0};
-  std::uint32_t S = 1;
-  const double* cur = src;
-  const std::uint32_t* cur_ids = src_ids;
-  std::uint64_t cur_stride = src_stride;
-  double* nxt = bufA;
-  std::uint32_t* nxt_ids = idsA;
-  int level = 0;
-  while (S > 0) {
-    if (level > 250) throw Error(GK_ERR_LOGIC, "BuildvEB_S: tree deeper than 250 levels");
-    const std::uint32_t off = lvl_off.back();
-    k_chunk_counts<<<blocks_for(S + 1), 256, 0, st>>>(na.count + off, S, chunk_cnt);
-    scratch.scan(chunk_cnt, chunk_off, S + 1);
-    k_chunk_node<<<std::min<unsigned>(blocks_for(n / kChunk + S), 4096), 256, 0, st>>>(chunk_off, S, chunk_node);
-    k_bbox_init<<<blocks_for(static_cast<std::uint64_t>(S) * D), 256, 0, st>>>(keys, S * D);
-    k_bbox<D><<<grid_w, 256, 0, st>>>(cur, cur_stride, chunk_off, chunk_node, S, off, na, keys);
-    k_split<D><<<blocks_for(S), 256, 0, st>>>(S, off, level, leaf, heuristic, keys, na);
-    k_count<D><<<grid_w, 256, 0, st>>>(cur, cur_ids, cur_stride, chunk_off, chunk_node, S, off, level, 0, na, chunk_left);
-    GK_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(std::uint32_t), st));
-    k_check<<<blocks_for(S + 1), 256, 0, st>>>(S, off, na, is_int, obj_list, counters);
-    scratch.scan(is_int, irank, S + 1);
-    GK_CUDA(cudaMemcpyAsync(counters + 1, irank + S, 4, cudaMemcpyDeviceToDevice, st));
-    GK_CUDA(cudaMemcpyAsync(counters + 2, chunk_off + S, 4, cudaMemcpyDeviceToDevice, st));
-    GK_CUDA(cudaMemcpyAsync(h_counters, counters, 3 * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, st));
-    GK_CUDA(cudaStreamSynchronize(st));
-    const std::uint32_t nobj = h_counters[0], nint = h_counters[1], nchunks = h_counters[2];
-    if (nobj > 0) {
-      if (nobj > sel_cap) {
-        dfree(sel, st);
-        dfree(hist, st);
-        sel_cap = std::max<std::uint64_t>(nobj, 2 * sel_cap);
-        sel = dalloc<SelState>(sel_cap, st);
-        hist = dalloc<std::uint32_t>(sel_cap * 256, st);
-      }
-      GK_CUDA(cudaMemsetAsync(hist, 0, static_cast<std::size_t>(nobj) * 256 * 4, st));
-      k_sel_init<<<blocks_for(nobj), 256, 0, st>>>(nobj, obj_list, na, sel);
-      for (int p = 0; p < 12; ++p) {
-        k_sel_hist<D><<<grid_w, 256, 0, st>>>(cur, cur_ids, cur_stride, chunk_off, chunk_node, S, off, level, p, na, sel,
-                                              hist);
-        k_sel_pick<<<blocks_for(nobj), 256, 0, st>>>(nobj, p, sel, hist);
-      }
-      k_sel_finish<<<blocks_for(nobj), 256, 0, st>>>(nobj, obj_list, sel, na);
-      k_count<D><<<grid_w, 256, 0, st>>>(cur, cur_ids, cur_stride, chunk_off, chunk_node, S, off, level, 1, na,
-                                         chunk_left);
-    }
-    scratch.scan(chunk_left, left_scan, static_cast<std::uint64_t>(nchunks) + 1);
-    const std::uint32_t next_off = off + S;
-    k_children<<<blocks_for(S), 256, 0, st>>>(S, off, next_off, irank, na);
-    k_scatter<D><<<grid_w, 256, 0, st>>>(cur, cur_ids, cur_stride, nxt, nxt_ids, T.coords, T.ids, n, chunk_off,
-                                         chunk_node, left_scan, S, off, level, na);
-    GK_CHECK_LAUNCH();
-    lvl_off.push_back(next_off);
-    S = 2 * nint;
-    ++level;
-    // ping-pong: the partitioned points now live in nxt (stride n)
-    cur = nxt;
-    cur_ids = nxt_ids;
-    cur_stride = n;
-    nxt = (nxt == bufA) ? bufB : bufA;
-    nxt_ids = (nxt_ids == idsA) ? idsB : idsA;
-  }
-  const int H = level;
-  const std::uint32_t N = lvl_off.back();
-  lvl_off.push_back(N);  // lvl_off[H+1] = N (so child_idx of an end position at level H-1 is defined)
-  T.height = H;
-  T.n_nodes = N;
-
-  // vEB slots, top-down
-  std::uint32_t* d_lvl_off = dalloc<std::uint32_t>(lvl_off.size(), st);
-  GK_CUDA(cudaMemcpyAsync(d_lvl_off, lvl_off.data(), lvl_off.size() * 4, cudaMemcpyHostToDevice, st));
-  GK_CUDA(cudaMemsetAsync(na.pos, 0, 4, st));
-  std::vector<std::pair<int, int>> cut(H + 1, {0, 0});
-  veb_cuts(0, H, cut);
-  for (int d = 1; d < H; ++d) {
-    const std::uint32_t Sd = lvl_off[d + 1] - lvl_off[d];
-    k_veb<<<blocks_for(Sd), 256, 0, st>>>(d, cut[d].first, cut[d].second, d_lvl_off, na);
-  }
-  std::uint32_t* int_by_slot = dalloc<std::uint32_t>(N + 1, st);
-  T.irank = dalloc<std::uint32_t>(N + 1, st);
-  k_slot_flags<<<blocks_for(N + 1), 256, 0, st>>>(N, na, int_by_slot);
-  scratch.scan(int_by_slot, T.irank, static_cast<std::uint64_t>(N) + 1);
-  T.n_internal = (N - 1) / 2;
-  T.canon = dalloc<gk_canon_node>(N, st);
-  T.tnodes = dalloc<TNode<D>>(T.n_internal, st);
-  T.orig = dalloc<std::int32_t>(3 * static_cast<std::uint64_t>(N), st);
-  GK_CUDA(cudaMemsetAsync(T.orig + 2 * static_cast<std::uint64_t>(N), 0xff, 4, st));  // parent(root) = -1
-  k_emit<D><<<blocks_for(N), 256, 0, st>>>(N, na, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
-  GK_CHECK_LAUNCH();
-  T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
-  T.root_slot = 0;
-
-  dfree(int_by_slot, st);
-  dfree(d_lvl_off, st);
-  dfree(bufA, st); dfree(bufB, st); dfree(idsA, st); dfree(idsB, st);
-  dfree(na.start, st); dfree(na.count, st); dfree(na.parent, st); dfree(na.cbase, st); dfree(na.nleft, st);
-  dfree(na.pos, st); dfree(na.thr_id, st); dfree(na.flags, st); dfree(na.level, st); dfree(na.split, st);
-  dfree(na.lo, st); dfree(na.hi, st);
-  dfree(chunk_cnt, st); dfree(chunk_off, st); dfree(chunk_node, st); dfree(chunk_left, st); dfree(left_scan, st);
-  dfree(is_int, st); dfree(irank, st); dfree(obj_list, st); dfree(keys, st); dfree(counters, st);
-  dfree(sel, st); dfree(hist, st);
-  GK_CUDA(cudaFreeHost(h_counters));
+inline unsigned blocks_for(std::uint64_t n, unsigned t = 256) {
+  return static_cast<unsigned>(std::max<std::uint64_t>(1, (n + t - 1) / t));
 }
 
 // ------------------------------------------------------------ Erase_S collapse --
@@ -697,8 +630,8 @@ __global__ void k_collapse_up(std::uint32_t N, const gk_canon_node* __restrict__
     if (p < 0) break;
     if (atomicAdd(&arrive[p], 1u) == 0) break;  // the sibling's thread finishes the parent
     __threadfence();
-    const std::int32_t a = __ldcg(&repl[orig[p]]), b = __ldcg(&repl[orig[N + p]]);
-    __stcg(&repl[p], (a >= 0 && b >= 0) ? p : (a >= 0 ? a : b));
+    const std::int32_t x = __ldcg(&repl[orig[p]]), y = __ldcg(&repl[orig[N + p]]);
+    __stcg(&repl[p], (x >= 0 && y >= 0) ? p : (x >= 0 ? x : y));
     cur = p;
   }
 }
@@ -708,12 +641,12 @@ __global__ void k_relink(std::uint32_t N, gk_canon_node* canon, TNode<D>* tn, co
                          const std::int32_t* __restrict__ orig, const std::int32_t* __restrict__ repl) {
   std::uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= N || canon[v].kind != 0) return;
-  const std::int32_t a = repl[orig[v]], b = repl[orig[N + v]];
-  if (a < 0 || b < 0) return;  // v itself is spliced out or removed
-  canon[v].left = a;
-  canon[v].right = b;
+  const std::int32_t x = repl[orig[v]], y = repl[orig[N + v]];
+  if (x < 0 || y < 0) return;  // v itself is spliced out or removed
+  canon[v].left = x;
+  canon[v].right = y;
   TNode<D> t = tn[irank[v]];
-  const std::int32_t ch[2] = {a, b};
+  const std::int32_t ch[2] = {x, y};
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const gk_canon_node& c = canon[ch[s]];
@@ -753,18 +686,149 @@ void collapse_d(DevTree& T, cudaStream_t st) {
   dfree(arrive, st);
 }
 
+// ------------------------------------------------------------------ driver --
+int coresident_blocks(const void* fn) {
+  int dev = 0, sms = 0, per = 0;
+  GK_CUDA(cudaGetDevice(&dev));
+  GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, 0));
+  return std::max(1, per) * sms;
+}
+
+template <int D>
+void build_tree_d(BuildScratch& sc, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                  const std::uint32_t* src_ids, std::uint64_t n, DevTree& T, cudaStream_t st) {
+  T = DevTree();
+  T.d = D;
+  T.n = n;
+  T.build_size = n;
+  T.live = n;
+  if (n == 0) return;
+  if (n >= 0x7fffffffULL) throw Error(GK_ERR_INVALID, "static tree larger than 2^31-2 points");
+  const std::uint64_t cap = 2 * n - 1;
+  const std::uint64_t cap_level = std::min<std::uint64_t>(cap, n);
+  const std::uint64_t cap_chunks = n / kChunk + cap_level + 2;
+
+  T.coords = dalloc<double>(n * D, st);
+  T.ids = dalloc<std::uint32_t>(n, st);
+
+  // grid: co-resident blocks, fewer for small trees (barriers are cheaper with fewer blocks)
+  static int maxb[9] = {0};
+  if (!maxb[D]) maxb[D] = coresident_blocks(reinterpret_cast<const void*>(k_build<D>));
+  const int G = static_cast<int>(std::min<std::uint64_t>(maxb[D], std::max<std::uint64_t>(1, n / 4096)));
+
+  BuildArgs a;
+  a.leaf = leaf;
+  a.heuristic = heuristic;
+  a.n = static_cast<std::uint32_t>(n);
+  a.src = src;
+  a.src_stride = src_stride;
+  a.src_ids = src_ids;
+  const std::size_t need = 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) +
+                           (cap_level + 1) * 4 * 5 + cap_chunks * 4 * 3 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 +
+                           C_COUNT * 4 + kSelCap * sizeof(SelState) + kSelCap * 256 * 4 + (G + 1) * 4 + 4 * (cap + 1) +
+                           40 * 256;
+  char* base = sc.reserve(need, st);
+  std::size_t used = 0;
+  auto take = [&](std::size_t bytes) -> char* {
+    used = (used + 255) & ~std::size_t(255);
+    char* p = base + used;
+    used += bytes;
+    return p;
+  };
+  a.bufA = reinterpret_cast<double*>(take(n * D * 8));
+  a.bufB = reinterpret_cast<double*>(take(n * D * 8));
+  a.idsA = reinterpret_cast<std::uint32_t*>(take(n * 4));
+  a.idsB = reinterpret_cast<std::uint32_t*>(take(n * 4));
+  a.out = T.coords;
+  a.out_ids = T.ids;
+  NodeArrays& na = a.na;
+  na.start = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+  na.count = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+  na.parent = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+  na.cbase = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+  na.nleft = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+  na.pos = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
+  na.thr_id = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+  na.flags = reinterpret_cast<std::uint8_t*>(take(cap));
+  na.level = reinterpret_cast<std::uint8_t*>(take(cap));
+  na.split = reinterpret_cast<double*>(take(cap * 8));
+  na.lo = reinterpret_cast<double*>(take(cap * D * 8));
+  na.hi = reinterpret_cast<double*>(take(cap * D * 8));
+  a.lvl_off = reinterpret_cast<std::uint32_t*>(take((kMaxLevels + 2) * 4));
+  a.ctrl = reinterpret_cast<std::uint32_t*>(take(C_COUNT * 4));
+  a.chunk_cnt = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.chunk_off = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.is_int = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.irank = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.obj_list = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.chunk_node = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
+  a.chunk_left = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
+  a.left_scan = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
+  a.keys = reinterpret_cast<unsigned long long*>(take(cap_level * D * 2 * 8));
+  a.sel = reinterpret_cast<SelState*>(take(kSelCap * sizeof(SelState)));
+  a.hist = reinterpret_cast<std::uint32_t*>(take(kSelCap * 256 * 4));
+  a.bsum = reinterpret_cast<std::uint32_t*>(take((G + 1) * 4));
+  a.int_by_slot = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
+  if (used > need) throw Error(GK_ERR_LOGIC, "BuildvEB_S scratch accounting");
+
+  void* args[] = {&a};
+  GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D>), dim3(G), dim3(kThreads), args, 0, st));
+  GK_CUDA(cudaMemcpyAsync(sc.host_ctrl, a.ctrl, C_COUNT * 4, cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  const int H = static_cast<int>(sc.host_ctrl[C_H]);
+  const std::uint32_t N = sc.host_ctrl[C_N];
+  if (H >= kMaxLevels) throw Error(GK_ERR_LOGIC, "BuildvEB_S: tree deeper than 256 levels");
+  T.height = H;
+  T.n_nodes = N;
+  T.n_internal = (N - 1) / 2;
+  T.irank = dalloc<std::uint32_t>(static_cast<std::uint64_t>(N) + 1, st);
+  T.canon = dalloc<gk_canon_node>(N, st);
+  T.tnodes = dalloc<TNode<D>>(T.n_internal, st);
+  T.orig = dalloc<std::int32_t>(3 * static_cast<std::uint64_t>(N), st);
+  GK_CUDA(cudaMemsetAsync(T.orig + 2 * static_cast<std::uint64_t>(N), 0xff, 4, st));  // parent(root) = -1
+  std::uint32_t* irank_ptr = T.irank;
+  void* args2[] = {&a, &irank_ptr};
+  const int G2 = static_cast<int>(std::min<std::uint64_t>(G, std::max<std::uint64_t>(1, N / 4096)));
+  GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_slot_rank), dim3(G2), dim3(kThreads), args2, 0, st));
+  k_emit<D><<<blocks_for(N), 256, 0, st>>>(a, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
+  GK_CHECK_LAUNCH();
+  T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
+  T.root_slot = 0;
+}
+
 }  // namespace
 
-void build_tree(int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride, const std::uint32_t* src_ids,
-                std::uint64_t n, DevTree& out, cudaStream_t st) {
+BuildScratch::~BuildScratch() {
+  if (base) cudaFree(base);
+  if (host_ctrl) cudaFreeHost(host_ctrl);
+}
+
+char* BuildScratch::reserve(std::size_t bytes, cudaStream_t st) {
+  if (!host_ctrl) GK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_ctrl), 64));
+  if (bytes > size) {
+    if (base) {
+      GK_CUDA(cudaStreamSynchronize(st));
+      GK_CUDA(cudaFree(base));
+      base = nullptr;
+    }
+    const std::size_t want = std::max(bytes, size + size / 2);
+    GK_CUDA(cudaMalloc(&base, want));
+    size = want;
+  }
+  return static_cast<char*>(base);
+}
+
+void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st) {
   switch (d) {
-    case 2: build_tree_d<2>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 3: build_tree_d<3>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 4: build_tree_d<4>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 5: build_tree_d<5>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 6: build_tree_d<6>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 7: build_tree_d<7>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 8: build_tree_d<8>(leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 2: build_tree_d<2>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 3: build_tree_d<3>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 4: build_tree_d<4>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 5: build_tree_d<5>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 6: build_tree_d<6>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 7: build_tree_d<7>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 8: build_tree_d<8>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
     default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
   }
 }

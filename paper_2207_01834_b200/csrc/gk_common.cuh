@@ -92,7 +92,16 @@ struct TreeSet {
 };
 
 // build.cu
-void build_tree(int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+// Grow-only device scratch for BuildvEB_S (one per handle; builds are serialised
+// on the handle's stream) plus a pinned control-word readback buffer.
+struct BuildScratch {
+  void* base = nullptr;
+  std::size_t size = 0;
+  std::uint32_t* host_ctrl = nullptr;
+  ~BuildScratch();
+  char* reserve(std::size_t bytes, cudaStream_t st);
+};
+void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st);
 void free_tree(DevTree& t, cudaStream_t st);
 // Erase_S collapse: after tombstoning, drop emptied leaves
