@@ -177,6 +177,7 @@ struct gk_bdl {
   std::uint32_t X = 1024, leaf = 16;
   int heuristic = 0, device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t pst[2] = {nullptr, nullptr};  // pipelined host-API kNN (copy/compute overlap)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<DevTree> statics = std::vector<DevTree>(64);
   std::uint64_t F = 0;
@@ -470,6 +471,7 @@ int gk_bdl_create(int dim, uint32_t X, uint32_t leaf, int heuristic, int device,
     h->device = device;
     try {
       GK_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+      for (auto& ps : h->pst) GK_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
       for (auto& e : h->ev) GK_CUDA(cudaEventCreate(&e));
       cudaMemPool_t pool;
       GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -498,6 +500,7 @@ int gk_bdl_destroy(gk_bdl* h) {
     if (h->cub_tmp) cudaFreeAsync(h->cub_tmp, h->st);
     cudaStreamSynchronize(h->st);
     for (auto& e : h->ev) cudaEventDestroy(e);
+    for (auto& ps : h->pst) cudaStreamDestroy(ps);
     cudaStreamDestroy(h->st);
     delete h;
   });
@@ -621,6 +624,15 @@ int gk_bdl_knn_counted_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k
   });
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, double* d2) {
   return guard([&] {
     need(h != nullptr, "null handle");
@@ -629,6 +641,37 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
     if (k > GK_MAX_K) throw Error(GK_ERR_UNSUPPORTED, "k > " + std::to_string(GK_MAX_K) + " is not supported");
     if (nq == 0) return;
     DevScope ds(h->device);
+    const TreeSet ts = h->trees();
+    const std::uint64_t kChunkQ = std::max<std::uint64_t>(1u << 20, (nq + 3) / 4);
+    if (ts.count > 0 && nq > kChunkQ && is_pinned(q) && is_pinned(ids) && is_pinned(d2)) {
+      // pinned host buffers: pipeline H2D(chunk i+1) | traversal(chunk i) | D2H(chunk i-1) on two streams
+      // (each chunk is Morton-ordered on its own; results are bit-identical to the one-shot path)
+      GK_CUDA(cudaStreamSynchronize(h->st));
+      double* dq[2];
+      std::uint32_t* di[2];
+      double* dd[2];
+      for (int s2 = 0; s2 < 2; ++s2) {
+        dq[s2] = dalloc<double>(kChunkQ * h->d, h->pst[s2]);
+        di[s2] = dalloc<std::uint32_t>(kChunkQ * k, h->pst[s2]);
+        dd[s2] = dalloc<double>(kChunkQ * k, h->pst[s2]);
+      }
+      int slot = 0;
+      for (std::uint64_t off = 0; off < nq; off += kChunkQ, slot ^= 1) {
+        const std::uint64_t m = std::min(kChunkQ, nq - off);
+        cudaStream_t s2 = h->pst[slot];
+        GK_CUDA(cudaMemcpyAsync(dq[slot], q + off * h->d, m * h->d * sizeof(double), cudaMemcpyHostToDevice, s2));
+        knn_launch(h->d, k, ts, dq[slot], m, di[slot], dd[slot], nullptr, s2, nullptr, nullptr);
+        GK_CUDA(cudaMemcpyAsync(ids + off * k, di[slot], m * k * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, s2));
+        GK_CUDA(cudaMemcpyAsync(d2 + off * k, dd[slot], m * k * sizeof(double), cudaMemcpyDeviceToHost, s2));
+      }
+      for (int s2 = 0; s2 < 2; ++s2) {
+        dfree(dq[s2], h->pst[s2]);
+        dfree(di[s2], h->pst[s2]);
+        dfree(dd[s2], h->pst[s2]);
+        GK_CUDA(cudaStreamSynchronize(h->pst[s2]));
+      }
+      return;
+    }
     double* dq = dalloc<double>(nq * h->d, h->st);
     std::uint32_t* di = dalloc<std::uint32_t>(nq * k, h->st);
     double* dd = dalloc<double>(nq * k, h->st);

@@ -293,6 +293,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const 
 }
 
 // --------------------------------------------------------------- K2: order --
+__global__ void k_qbox_init(unsigned long long* box, int d) {
+  if (threadIdx.x < d) { box[2 * threadIdx.x] = ~0ULL; box[2 * threadIdx.x + 1] = 0ULL; }
+}
+
 template <int D>
 __global__ void k_qbox(const double* __restrict__ Q, std::uint64_t nq, unsigned long long* box) {
   double lo[D], hi[D];
@@ -395,9 +399,7 @@ void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, c
   GK_CUDA(cudaMallocAsync(&keys, nq * 4, st));
   GK_CUDA(cudaMallocAsync(&keys2, nq * 4, st));
   GK_CUDA(cudaMallocAsync(&idx, nq * 4, st));
-  std::vector<unsigned long long> init(2 * D);
-  for (int j = 0; j < D; ++j) { init[2 * j] = ~0ULL; init[2 * j + 1] = 0ULL; }
-  GK_CUDA(cudaMemcpyAsync(box, init.data(), init.size() * 8, cudaMemcpyHostToDevice, st));
+  k_qbox_init<<<1, 32, 0, st>>>(box, D);
   const unsigned gb = static_cast<unsigned>(std::min<std::uint64_t>((nq + 255) / 256, 148 * 8));
   k_qbox<D><<<gb, 256, 0, st>>>(Q, nq, box);
   k_morton<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, box, keys, idx);

@@ -268,3 +268,20 @@ def test_full_c1_self_queries(gk, oracle):
     o.insert(P)
     assert_struct_equal(g, o, trees=True)
     assert_knn_equal((ids[rows], d2[rows]), o.knn(P[rows], 5), "C1 full sampled")
+
+
+def test_pinned_pipelined_host_knn(gk):
+    """host API with pinned buffers takes the chunked copy/compute pipeline: results identical"""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(12)
+    P = rng.random((300000, 3))
+    Q = rng.random((2_600_000, 3))
+    g = gk.BDLTree(3)
+    g.insert(P)
+    ids0, d20 = g.knn(Q, 8)  # pageable: one-shot path
+    Qp = torch.from_numpy(Q).pin_memory().numpy()
+    ids = torch.empty((len(Q), 8), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    d2 = torch.empty((len(Q), 8), dtype=torch.float64).pin_memory().numpy()
+    rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, len(Q), 8, ids.ctypes.data, d2.ctypes.data)
+    assert rc == 0
+    assert np.array_equal(ids, ids0) and np.array_equal(d2, d20)
