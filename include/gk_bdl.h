@@ -113,6 +113,10 @@ int gk_bdl_info_get(gk_bdl* h, gk_bdl_info* info);
  * vEB slot order, ids and AoS points in leaf order.  Pass NULL to query sizes. */
 int gk_bdl_tree_export(gk_bdl* h, int tree, gk_canon_node* nodes, uint32_t* ids, double* pts,
                        uint64_t* n_nodes, uint64_t* n_pts);
+/* Bloom prefilter of static tree `tree` (built lazily, 10 bits/key, 7 probes;
+ * PAPER.md:1468-1475): may_contain[i] = 0 means point i is
+ * definitely not in the tree.  Erase_L uses the same filters internally. */
+int gk_bdl_bloom_query(gk_bdl* h, int tree, const double* pts, uint64_t n, uint8_t* may_contain);
 /* Stream the handle runs on (cudaStream_t), e.g. to time with events. */
 void* gk_bdl_stream(gk_bdl* h);
 int gk_bdl_sync(gk_bdl* h);

@@ -77,6 +77,7 @@ def lib():
         L.gk_bdl_knn_counted_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, C.POINTER(KnnCounters)]
         L.gk_bdl_info_get.argtypes = [_P, C.POINTER(_Info)]
         L.gk_bdl_tree_export.argtypes = [_P, C.c_int, _P, _P, _P, C.POINTER(_u64), C.POINTER(_u64)]
+        L.gk_bdl_bloom_query.argtypes = [_P, C.c_int, _P, _u64, _P]
         L.gk_bdl_stream.restype = _P
         L.gk_bdl_stream.argtypes = [_P]
         L.gk_bdl_sync.argtypes = [_P]
@@ -215,6 +216,13 @@ class BDLTree:
         _check(lib().gk_bdl_tree_export(self._h, int(tree), _ptr(nodes), _ptr(ids), _ptr(pts), C.byref(nn),
                                         C.byref(npt)))
         return nodes, ids, pts
+
+    def bloom_may_contain(self, tree: int, pts) -> np.ndarray:
+        """bloom prefilter of static tree `tree`: False = definitely absent"""
+        a = _rows(pts, self.d)
+        out = np.zeros(a.shape[0], np.uint8)
+        _check(lib().gk_bdl_bloom_query(self._h, int(tree), _ptr(a), a.shape[0], _ptr(out)))
+        return out.astype(bool)
 
     def stream(self) -> int:
         return int(lib().gk_bdl_stream(self._h) or 0)

@@ -112,6 +112,26 @@ __global__ void k_buffer_dead(const double* __restrict__ tree_c0, const std::uin
   if (i < n && isnan(tree_c0[i])) flags[src_idx[i]] = 0u;
 }
 
+// lazy bloom construction over a tree's live points (parallel over the point range)
+__global__ void k_bloom_build(const double* __restrict__ coords, std::uint64_t n, int d, std::uint64_t* bits,
+                              std::uint64_t m) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n || isnan(coords[i])) return;
+  const std::uint64_t key = bloom_key(coords + i, d, n);
+  const std::uint64_t h1 = key, h2 = bloom_mix(key ^ 0x5851f42d4c957f2dULL) | 1ULL;
+  for (int k = 0; k < kBloomHashes; ++k) {
+    const std::uint64_t b = (h1 + static_cast<std::uint64_t>(k) * h2) % m;
+    atomicOr(reinterpret_cast<unsigned long long*>(&bits[b >> 6]), 1ULL << (b & 63));
+  }
+}
+
+__global__ void k_bloom_query(const std::uint64_t* __restrict__ bits, std::uint64_t m, const double* __restrict__ P, int d,
+                              std::uint64_t n, std::uint8_t* out) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  out[i] = bloom_test(bits, m, bloom_key(P + i * d, d, 1)) ? 1 : 0;
+}
+
 // Erase_S for every tree at once: one thread per erase point walks each tree
 // along the children whose (conservative) box contains the point and
 // tombstones coordinate-exact matches with a CAS on coordinate 0 (so every
@@ -130,7 +150,9 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
     pf_hi[j] = __double2float_ru(p[j]);
   }
   std::uint64_t stk[kStack];
+  const std::uint64_t key = bloom_key_reg<D>(p);
   for (int t = 0; t < ts.count; ++t) {
+    if (ts.t[t].bloom && !bloom_test(ts.t[t].bloom, ts.t[t].bloom_bits, key)) continue;  // definitely absent
     const TNode<D>* nodes = static_cast<const TNode<D>*>(ts.t[t].tnodes);
     double* coords = const_cast<double*>(ts.t[t].coords);
     const std::uint64_t stride = ts.t[t].stride;
@@ -310,6 +332,17 @@ struct gk_bdl {
     built_pts = built_pts_now;
   }
 
+  // bloom filters are built lazily, on the first erase that touches the tree
+  void ensure_bloom(DevTree& T) {
+    if (T.bloom || T.n == 0) return;
+    const std::uint64_t m = std::max<std::uint64_t>(64, ((T.n * kBloomBitsPerKey + 63) / 64) * 64);
+    T.bloom = dalloc<std::uint64_t>(m / 64, st);
+    T.bloom_bits = m;
+    GK_CUDA(cudaMemsetAsync(T.bloom, 0, m / 8, st));
+    k_bloom_build<<<blocks_for(T.n), 256, 0, st>>>(T.coords, T.n, d, T.bloom, m);
+    GK_CHECK_LAUNCH();
+  }
+
   TreeSet trees(bool include_buffer = true) const {
     TreeSet ts{};
     ts.count = 0;
@@ -330,8 +363,9 @@ struct gk_bdl {
     TreeSet ts{};
     for (int i = 63; i >= 0; --i)
       if ((F >> i & 1ULL) && statics[i].live > 0) {
-        const DevTree& T = statics[i];
-        ts.t[ts.count++] = TreeRef{T.tnodes, T.coords, T.ids, T.n, T.root_ref};
+        DevTree& T = statics[i];
+        ensure_bloom(T);
+        ts.t[ts.count++] = TreeRef{T.tnodes, T.coords, T.ids, T.n, T.root_ref, T.bloom, T.bloom_bits};
         which.push_back(i);
       }
     if (buf_n > 0) {
@@ -731,6 +765,27 @@ int gk_bdl_tree_export(gk_bdl* h, int tree, gk_canon_node* nodes, uint32_t* ids,
     if (pts)
       for (std::uint64_t i = 0; i < T->n; ++i)
         for (int j = 0; j < h->d; ++j) pts[i * h->d + j] = soa[j * T->n + i];
+  });
+}
+
+int gk_bdl_bloom_query(gk_bdl* h, int tree, const double* pts, uint64_t n, uint8_t* may_contain) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(tree >= 0 && tree < 64 && (h->F >> tree & 1ULL), "static tree does not exist");
+    need(n == 0 || (pts && may_contain), "null buffer");
+    if (n == 0) return;
+    DevScope ds(h->device);
+    DevTree& T = h->statics[tree];
+    h->ensure_bloom(T);
+    double* dp = dalloc<double>(n * h->d, h->st);
+    std::uint8_t* dm = dalloc<std::uint8_t>(n, h->st);
+    GK_CUDA(cudaMemcpyAsync(dp, pts, n * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    k_bloom_query<<<blocks_for(n), 256, 0, h->st>>>(T.bloom, T.bloom_bits, dp, h->d, n, dm);
+    GK_CHECK_LAUNCH();
+    GK_CUDA(cudaMemcpyAsync(may_contain, dm, n, cudaMemcpyDeviceToHost, h->st));
+    dfree(dp, h->st);
+    dfree(dm, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
   });
 }
 

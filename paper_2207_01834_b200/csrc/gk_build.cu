@@ -854,6 +854,7 @@ void free_tree(DevTree& t, cudaStream_t st) {
   dfree(t.canon, st);
   dfree(t.orig, st);
   dfree(t.irank, st);
+  dfree(t.bloom, st);
   t = DevTree();
 }
 

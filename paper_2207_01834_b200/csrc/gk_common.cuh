@@ -73,6 +73,8 @@ struct DevTree {
   std::int32_t* orig = nullptr;   // build-time topology per slot: [left | right | parent] (3 x n_nodes)
   std::uint32_t* irank = nullptr; // slot -> internal rank (TNode index), n_nodes + 1
   std::int32_t root_slot = 0;     // -1 once Erase_S removed every point
+  std::uint64_t* bloom = nullptr; // lazily built erase prefilter, bloom_bits bits
+  std::uint64_t bloom_bits = 0;
   int height = 0;
   std::uint64_t build_size = 0, live = 0;
 };
@@ -84,7 +86,47 @@ struct TreeRef {
   const std::uint32_t* ids;
   std::uint64_t stride;
   std::uint64_t root;
+  const std::uint64_t* bloom = nullptr;  // erase only; nullptr = no prefilter
+  std::uint64_t bloom_bits = 0;
 };
+
+// Bloom filter over points (10 bits/key, 7 probes; SPEC.md:599-606 parameters):
+// the key hashes all d coordinates with -0 canonicalised to +0 (erase matches by
+// value, so -0 and +0 must probe the same bits).
+constexpr int kBloomHashes = 7;
+constexpr int kBloomBitsPerKey = 10;
+__host__ __device__ inline std::uint64_t bloom_mix(std::uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ inline std::uint64_t bloom_key(const double* x, int d, std::uint64_t stride) {
+  std::uint64_t z = 0x243f6a8885a308d3ULL;
+  for (int j = 0; j < d; ++j) {
+    const double v = x[j * stride] == 0.0 ? 0.0 : x[j * stride];
+    z = bloom_mix(z ^ static_cast<std::uint64_t>(__double_as_longlong(v)));
+  }
+  return z;
+}
+template <int D>
+__device__ inline std::uint64_t bloom_key_reg(const double (&x)[D]) {
+  std::uint64_t z = 0x243f6a8885a308d3ULL;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double v = x[j] == 0.0 ? 0.0 : x[j];
+    z = bloom_mix(z ^ static_cast<std::uint64_t>(__double_as_longlong(v)));
+  }
+  return z;
+}
+__device__ inline bool bloom_test(const std::uint64_t* bits, std::uint64_t m, std::uint64_t key) {
+  const std::uint64_t h1 = key, h2 = bloom_mix(key ^ 0x5851f42d4c957f2dULL) | 1ULL;
+  for (int i = 0; i < kBloomHashes; ++i) {
+    const std::uint64_t b = (h1 + static_cast<std::uint64_t>(i) * h2) % m;
+    if (!((bits[b >> 6] >> (b & 63)) & 1ULL)) return false;
+  }
+  return true;
+}
 constexpr int kMaxTrees = 66;
 struct TreeSet {
   TreeRef t[kMaxTrees];

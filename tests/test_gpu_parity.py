@@ -285,3 +285,18 @@ def test_pinned_pipelined_host_knn(gk):
     rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, len(Q), 8, ids.ctypes.data, d2.ctypes.data)
     assert rc == 0
     assert np.array_equal(ids, ids0) and np.array_equal(d2, d20)
+
+
+def test_bloom_filter(gk):
+    """SPEC.md:604-606 / acceptance 10: no false negatives over 1e5 keys, FP <= 2% at 10 bits/key, h = 7"""
+    rng = np.random.default_rng(2022)
+    P = rng.random((100000, 3))
+    g = gk.BDLTree(3, X=100000)
+    g.insert(P)
+    assert g.info()["F"] == 1
+    assert g.bloom_may_contain(0, P).all()                      # no false negatives
+    fp = g.bloom_may_contain(0, rng.random((200000, 3))).mean()
+    assert fp <= 0.02, fp
+    g2 = gk.BDLTree(3, X=4)
+    g2.insert(np.array([[0.0, -0.0, 1.0]] * 4))
+    assert g2.bloom_may_contain(0, np.array([[-0.0, 0.0, 1.0]])).all()  # -0 == +0 probes the same bits
