@@ -89,7 +89,7 @@ __device__ __forceinline__ double leaf_d2(const double (&q)[D], const double* sp
 }
 
 template <int D, int K, bool COUNT>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_knn(const TreeSet ts, const double* __restrict__ Q,
+__global__ void __launch_bounds__(kWarps * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
                                                         unsigned long long* __restrict__ counters,
