@@ -97,6 +97,10 @@ __global__ void __launch_bounds__(kWarps * 32, (D <= 4 ? 5 : 4)) k_knn(const Tre
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
+  constexpr bool kPairMode = D >= 5;  // leaf work dominates at high D (C3: ~8x packet union)
+  constexpr int kPairLanes = 10;      // <= this many needing lanes: pair-parallel leaf scan
+  __shared__ double s_q[kWarps][kPairMode ? D * 32 : 1];       // the tile's queries, [D][lane]
+  __shared__ std::uint8_t s_own[kWarps][32];                   // lanes needing the current leaf
   // per-lane sorted top-K, one column per thread (conflict-free): [K][blockDim] d2, then [K][blockDim] ids
   extern __shared__ double s_cand[];
   double* cdv = s_cand + threadIdx.x;
@@ -134,6 +138,7 @@ __global__ void __launch_bounds__(kWarps * 32, (D <= 4 ? 5 : 4)) k_knn(const Tre
   for (int j = 0; j < D; ++j) {
     qlo[j] = __double2float_rd(q[j]);
     qhi[j] = __double2float_ru(q[j]);
+    if (kPairMode) s_q[w][j * 32 + lane] = q[j];
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) {
@@ -187,12 +192,55 @@ __global__ void __launch_bounds__(kWarps * 32, (D <= 4 ? 5 : 4)) k_knn(const Tre
           s_pts[w][lane] = __longlong_as_double(0x7ff8000000000000LL);  // NaN pad: never enters the top-k
         }
         __syncwarp();
-        // two independent distance chains per iteration (fp64 latency)
-        for (std::uint32_t p = 0; p < c; p += 2) {
-          const double da = leaf_d2<D>(q, s_pts[w], p);
-          const double db = leaf_d2<D>(q, s_pts[w], p + 1);
-          offer(da, s_ids[w][p]);
-          offer(db, s_ids[w][p + 1]);
+        const unsigned needm = __ballot_sync(0xffffffffu, need);
+        const int m = __popc(needm);
+        if (!kPairMode || m > kPairLanes) {
+          // each lane scans all points against its own query,
+          // two independent distance chains per iteration (fp64 latency)
+          for (std::uint32_t p = 0; p < c; p += 2) {
+            const double da = leaf_d2<D>(q, s_pts[w], p);
+            const double db = leaf_d2<D>(q, s_pts[w], p + 1);
+            offer(da, s_ids[w][p]);
+            offer(db, s_ids[w][p + 1]);
+          }
+        } else if (m > 0) {
+          // high D, few lanes need this leaf: spread the m x c needed (query, point) pairs
+          // over the warp; a pair that beats its owner's k-th distance goes to the owner lane
+          if (need) s_own[w][__popc(needm & ((1u << lane) - 1u))] = static_cast<std::uint8_t>(lane);
+          __syncwarp();
+          const std::uint32_t total = static_cast<std::uint32_t>(m) * c;
+          const std::uint32_t dqi = 32u / c, dp = 32u % c;
+          std::uint32_t qi = static_cast<std::uint32_t>(lane) / c, pp = static_cast<std::uint32_t>(lane) % c;
+          for (std::uint32_t t0 = 0; t0 < total; t0 += 32) {
+            int own = 0;
+            double d2 = 0.0;
+            bool cand = false;
+            if (t0 + lane < total) {
+              own = s_own[w][qi];
+              const double* qo = &s_q[w][own];
+              const double t = __dsub_rn(qo[0], s_pts[w][pp]);
+              d2 = __dmul_rn(t, t);
+#pragma unroll
+              for (int j = 1; j < D; ++j) {
+                const double tt = __dsub_rn(qo[j * 32], s_pts[w][j * GK_MAX_LEAF + pp]);
+                d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
+              }
+              cand = d2 <= s_cand[(K - 1) * CS + w * 32 + own];
+            }
+            unsigned bal = __ballot_sync(0xffffffffu, cand);
+            while (bal) {
+              const int b = __ffs(bal) - 1;
+              bal &= bal - 1;
+              const int ob = __shfl_sync(0xffffffffu, own, b);
+              const double db = __shfl_sync(0xffffffffu, d2, b);
+              const std::uint32_t pb = __shfl_sync(0xffffffffu, pp, b);
+              if (lane == ob) offer(db, s_ids[w][pb]);
+            }
+            __syncwarp();
+            pp += dp;
+            qi += dqi;
+            if (pp >= c) { pp -= c; ++qi; }
+          }
         }
         if (COUNT) {
           if (need) { c_leaves++; c_dists += c; }
