@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -213,7 +214,11 @@ struct gk_bdl {
   std::uint64_t built_pts = 0;
   void* cub_tmp = nullptr;
   std::size_t cub_bytes = 0;
-  BuildScratch scratch;
+  BuildScratch scratch;                 // buffer-tree rebuilds (on st)
+  static constexpr int kBuildSlots = 4;  // concurrent builds of distinct new trees
+  BuildScratch bscratch[kBuildSlots];
+  cudaStream_t bst[kBuildSlots] = {};
+  cudaEvent_t ev_pool = nullptr;
 
   std::uint64_t bstride() const { return 2ULL * X; }
 
@@ -305,11 +310,12 @@ struct gk_bdl {
     }
     GK_CHECK_LAUNCH();
     if (r || drained) rebuild_buffer_tree();
-    // build the new trees, largest first, from contiguous pool slices
+    // build the new trees, largest first, from contiguous pool slices; distinct trees
+    // build concurrently on their own streams
     F = Fn;
+    std::vector<int> order;
+    std::vector<std::uint64_t> offs, cnts;
     std::uint64_t o = 0;
-    GK_CUDA(cudaEventRecord(ev[2], st));
-    std::uint64_t built_pts_now = 0;
     for (int i = 63; i >= 0; --i) {
       if (!(built >> i & 1ULL)) continue;
       const std::uint64_t cap = static_cast<std::uint64_t>(X) << i;
@@ -318,18 +324,29 @@ struct gk_bdl {
         F &= ~(1ULL << i);
         continue;
       }
-      build_tree(scratch, d, static_cast<int>(leaf), heuristic, pool + o, pool_n, pool_ids + o, c, statics[i], st);
+      order.push_back(i);
+      offs.push_back(o);
+      cnts.push_back(c);
       o += c;
-      built_pts_now += c;
     }
-    GK_CUDA(cudaEventRecord(ev[3], st));
+    const auto t0 = std::chrono::steady_clock::now();
+    GK_CUDA(cudaEventRecord(ev_pool, st));
+    for (std::size_t w0 = 0; w0 < order.size(); w0 += kBuildSlots) {
+      const std::size_t w1 = std::min(order.size(), w0 + kBuildSlots);
+      for (std::size_t t = w0; t < w1; ++t) {
+        const int slot = static_cast<int>(t - w0);
+        GK_CUDA(cudaStreamWaitEvent(bst[slot], ev_pool, 0));
+        build_begin(bscratch[slot], d, static_cast<int>(leaf), heuristic, pool + offs[t], pool_n, pool_ids + offs[t],
+                    cnts[t], statics[order[t]], bst[slot]);
+      }
+      for (std::size_t t = w0; t < w1; ++t) build_finish(bscratch[t - w0]);
+    }
+    for (auto& bs : bst) GK_CUDA(cudaStreamSynchronize(bs));
+    build_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    built_pts = o;
     dfree(pool, st);
     dfree(pool_ids, st);
     GK_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    GK_CUDA(cudaEventElapsedTime(&ms, ev[2], ev[3]));
-    build_ms = ms;
-    built_pts = built_pts_now;
   }
 
   // bloom filters are built lazily, on the first erase that touches the tree
@@ -506,6 +523,8 @@ int gk_bdl_create(int dim, uint32_t X, uint32_t leaf, int heuristic, int device,
     try {
       GK_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
       for (auto& ps : h->pst) GK_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+      for (auto& bs : h->bst) GK_CUDA(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+      GK_CUDA(cudaEventCreateWithFlags(&h->ev_pool, cudaEventDisableTiming));
       for (auto& e : h->ev) GK_CUDA(cudaEventCreate(&e));
       cudaMemPool_t pool;
       GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -535,6 +554,8 @@ int gk_bdl_destroy(gk_bdl* h) {
     cudaStreamSynchronize(h->st);
     for (auto& e : h->ev) cudaEventDestroy(e);
     for (auto& ps : h->pst) cudaStreamDestroy(ps);
+    for (auto& bs : h->bst) cudaStreamDestroy(bs);
+    cudaEventDestroy(h->ev_pool);
     cudaStreamDestroy(h->st);
     delete h;
   });

@@ -696,8 +696,10 @@ int coresident_blocks(const void* fn) {
 }
 
 template <int D>
-void build_tree_d(BuildScratch& sc, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                  const std::uint32_t* src_ids, std::uint64_t n, DevTree& T, cudaStream_t st) {
+void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                   const std::uint32_t* src_ids, std::uint64_t n, DevTree& T, cudaStream_t st) {
+  static_assert(sizeof(BuildArgs) <= sizeof(sc.args), "BuildScratch::args too small");
+  sc.pending = false;
   T = DevTree();
   T.d = D;
   T.n = n;
@@ -717,7 +719,8 @@ void build_tree_d(BuildScratch& sc, int leaf, int heuristic, const double* src, 
   if (!maxb[D]) maxb[D] = coresident_blocks(reinterpret_cast<const void*>(k_build<D>));
   const int G = static_cast<int>(std::min<std::uint64_t>(maxb[D], std::max<std::uint64_t>(1, n / 4096)));
 
-  BuildArgs a;
+  BuildArgs& a = *reinterpret_cast<BuildArgs*>(sc.args);
+  a = BuildArgs();
   a.leaf = leaf;
   a.heuristic = heuristic;
   a.n = static_cast<std::uint32_t>(n);
@@ -775,6 +778,22 @@ void build_tree_d(BuildScratch& sc, int leaf, int heuristic, const double* src, 
   void* args[] = {&a};
   GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D>), dim3(G), dim3(kThreads), args, 0, st));
   GK_CUDA(cudaMemcpyAsync(sc.host_ctrl, a.ctrl, C_COUNT * 4, cudaMemcpyDeviceToHost, st));
+  sc.d = D;
+  sc.grid = G;
+  sc.n = n;
+  sc.out = &T;
+  sc.st = st;
+  sc.pending = true;
+}
+
+template <int D>
+void build_finish_d(BuildScratch& sc) {
+  sc.pending = false;
+  BuildArgs& a = *reinterpret_cast<BuildArgs*>(sc.args);
+  DevTree& T = *sc.out;
+  cudaStream_t st = sc.st;
+  const std::uint64_t n = sc.n;
+  const int G = sc.grid;
   GK_CUDA(cudaStreamSynchronize(st));
   const int H = static_cast<int>(sc.host_ctrl[C_H]);
   const std::uint32_t N = sc.host_ctrl[C_N];
@@ -795,41 +814,49 @@ void build_tree_d(BuildScratch& sc, int leaf, int heuristic, const double* src, 
   GK_CHECK_LAUNCH();
   T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
   T.root_slot = 0;
+  GK_CUDA(cudaFreeAsync(sc.base, st));
+  sc.base = nullptr;
 }
 
 }  // namespace
 
 BuildScratch::~BuildScratch() {
-  if (base) cudaFree(base);
   if (host_ctrl) cudaFreeHost(host_ctrl);
 }
 
+// stream-ordered scratch from the device memory pool (cached across builds and handles)
 char* BuildScratch::reserve(std::size_t bytes, cudaStream_t st) {
   if (!host_ctrl) GK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_ctrl), 64));
-  if (bytes > size) {
-    if (base) {
-      GK_CUDA(cudaStreamSynchronize(st));
-      GK_CUDA(cudaFree(base));
-      base = nullptr;
-    }
-    const std::size_t want = std::max(bytes, size + size / 2);
-    GK_CUDA(cudaMalloc(&base, want));
-    size = want;
-  }
+  GK_CUDA(cudaMallocAsync(&base, bytes, st));
+  size = bytes;
   return static_cast<char*>(base);
 }
 
-void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st) {
+void build_begin(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st) {
   switch (d) {
-    case 2: build_tree_d<2>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 3: build_tree_d<3>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 4: build_tree_d<4>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 5: build_tree_d<5>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 6: build_tree_d<6>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 7: build_tree_d<7>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 8: build_tree_d<8>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 2: build_begin_d<2>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 3: build_begin_d<3>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 4: build_begin_d<4>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 5: build_begin_d<5>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 6: build_begin_d<6>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 7: build_begin_d<7>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 8: build_begin_d<8>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
     default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+void build_finish(BuildScratch& sc) {
+  if (!sc.pending) return;
+  switch (sc.d) {
+    case 2: build_finish_d<2>(sc); break;
+    case 3: build_finish_d<3>(sc); break;
+    case 4: build_finish_d<4>(sc); break;
+    case 5: build_finish_d<5>(sc); break;
+    case 6: build_finish_d<6>(sc); break;
+    case 7: build_finish_d<7>(sc); break;
+    case 8: build_finish_d<8>(sc); break;
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension");
   }
 }
 

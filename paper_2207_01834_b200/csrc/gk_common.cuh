@@ -134,17 +134,32 @@ struct TreeSet {
 };
 
 // build.cu
-// Grow-only device scratch for BuildvEB_S (one per handle; builds are serialised
-// on the handle's stream) plus a pinned control-word readback buffer.
+// Grow-only device scratch for BuildvEB_S plus a pinned control-word readback
+// buffer.  One build can be in flight per scratch: build_begin launches the
+// cooperative build kernel on `st` (asynchronously), build_finish waits for it,
+// sizes the node arrays and emits them.  Builds of distinct trees on distinct
+// (stream, scratch) pairs run concurrently (PAPER.md:1193 builds new trees in parallel).
 struct BuildScratch {
   void* base = nullptr;
   std::size_t size = 0;
   std::uint32_t* host_ctrl = nullptr;
+  alignas(16) unsigned char args[640];  // the in-flight build's kernel arguments
+  int d = 0, grid = 0;
+  std::uint64_t n = 0;
+  DevTree* out = nullptr;
+  cudaStream_t st = nullptr;
+  bool pending = false;
   ~BuildScratch();
   char* reserve(std::size_t bytes, cudaStream_t st);
 };
-void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st);
+void build_begin(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st);
+void build_finish(BuildScratch& sc);
+inline void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
+                       const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st) {
+  build_begin(sc, d, leaf, heuristic, src, src_stride, src_ids, n, out, st);
+  build_finish(sc);
+}
 void free_tree(DevTree& t, cudaStream_t st);
 // Erase_S collapse: after tombstoning, drop emptied leaves
 // and splice out internal nodes left with one child; relinks the canonical
