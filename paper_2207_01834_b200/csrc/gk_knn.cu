@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "gk_common.cuh"
@@ -32,7 +33,10 @@
 namespace gk {
 namespace {
 
-constexpr int kWarps = 8;  // 256 threads per block
+// warps per block: 8, or 4 for K > 16 so the shared-memory k-buffers (12 B x K per lane) still
+// leave room for several blocks per SM
+template <int K>
+__host__ __device__ constexpr int warps_for() { return K > 16 ? 4 : 8; }
 
 __device__ __forceinline__ bool lexlt(double a, std::uint32_t ia, double b, std::uint32_t ib) {
   return a < b || (a == b && ia < ib);
@@ -89,11 +93,12 @@ __device__ __forceinline__ double leaf_d2(const double (&q)[D], const double* sp
 }
 
 template <int D, int K, bool COUNT>
-__global__ void __launch_bounds__(kWarps * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
+__global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
                                                         unsigned long long* __restrict__ counters,
                                                         unsigned* __restrict__ tile_ctr) {
+  constexpr int kWarps = warps_for<K>();
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
@@ -401,22 +406,20 @@ __global__ void k_morton(const double* __restrict__ Q, std::uint64_t nq, const u
 template <int D, int K>
 void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, int k, std::uint32_t* ids,
               double* d2, unsigned long long* ctr, cudaStream_t st) {
+  constexpr int kWarps = warps_for<K>();
   const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
   const int smem = K * kWarps * 32 * 12;  // per-lane top-K columns
-  static bool configured = false;  // per (D, K) instantiation
-  if (!configured) {
+  static std::once_flag once;             // per (D, K) instantiation
+  static int resident = 0;                // co-resident blocks at this smem size
+  std::call_once(once, [&] {
     GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  static int resident = 0;  // blocks per SM at this smem size
-  if (!resident) {
     int dev = 0, sms = 0, per = 0;
     GK_CUDA(cudaGetDevice(&dev));
     GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn<D, K, false>, kWarps * 32, smem));
     resident = std::max(1, per) * sms;
-  }
+  });
   const unsigned grid = std::min<unsigned>(blocks, static_cast<unsigned>(resident));
   unsigned* tile_ctr = nullptr;
   GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
