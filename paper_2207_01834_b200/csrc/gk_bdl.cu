@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -697,7 +698,10 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
     if (nq == 0) return;
     DevScope ds(h->device);
     const TreeSet ts = h->trees();
-    const std::uint64_t kChunkQ = std::max<std::uint64_t>(1u << 20, (nq + 3) / 4);
+    // pipeline depth (tunable for experiments via GK_PIPE_CHUNKS; default 4)
+    std::uint64_t nchunk = 4;
+    if (const char* e = std::getenv("GK_PIPE_CHUNKS")) nchunk = std::max<std::uint64_t>(1, std::strtoull(e, nullptr, 10));
+    const std::uint64_t kChunkQ = std::max<std::uint64_t>(1u << 18, (nq + nchunk - 1) / nchunk);
     if (ts.count > 0 && nq > kChunkQ && is_pinned(q) && is_pinned(ids) && is_pinned(d2)) {
       // pinned host buffers: pipeline H2D(chunk i+1) | traversal(chunk i) | D2H(chunk i-1) on two streams
       // (each chunk is Morton-ordered on its own; results are bit-identical to the one-shot path)
