@@ -92,6 +92,25 @@ __device__ __forceinline__ double leaf_d2(const double (&q)[D], const double* sp
   return d2;
 }
 
+// distances of the query to staged leaf points p and p+1 (p even): one 16-byte shared
+// load per coordinate serves both, two independent fp64 chains
+template <int D>
+__device__ __forceinline__ void leaf_d2_pair(const double (&q)[D], const double* sp, std::uint32_t p, double& da,
+                                             double& db) {
+  double2 x = reinterpret_cast<const double2*>(sp)[p >> 1];
+  double ta = __dsub_rn(q[0], x.x), tb = __dsub_rn(q[0], x.y);
+  da = __dmul_rn(ta, ta);  // 0 + t0^2 == t0^2 exactly
+  db = __dmul_rn(tb, tb);
+#pragma unroll
+  for (int j = 1; j < D; ++j) {
+    x = reinterpret_cast<const double2*>(sp + j * GK_MAX_LEAF)[p >> 1];
+    ta = __dsub_rn(q[j], x.x);
+    tb = __dsub_rn(q[j], x.y);
+    da = __dadd_rn(da, __dmul_rn(ta, ta));
+    db = __dadd_rn(db, __dmul_rn(tb, tb));
+  }
+}
+
 template <int D, int K, bool COUNT>
 __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
@@ -100,7 +119,7 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
                                                         unsigned* __restrict__ tile_ctr) {
   constexpr int kWarps = warps_for<K>();
   __shared__ std::uint64_t s_stack[kWarps][kStack];
-  __shared__ double s_pts[kWarps][D * GK_MAX_LEAF];
+  __shared__ __align__(16) double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
   constexpr bool kPairMode = D >= 5;  // leaf work dominates at high D (C3: ~8x packet union)
   constexpr int kPairLanes = 10;      // <= this many needing lanes: pair-parallel leaf scan
@@ -155,8 +174,10 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
   // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
   float kthf = active ? __int_as_float(0x7f800000) : -1.f;
 
-  auto offer = [&](double d2, std::uint32_t pid) {
+  // offer staged leaf point p (distance d2) to this lane's k-buffer
+  auto offer = [&](double d2, std::uint32_t p) {
     if (d2 <= kd) {  // rare: lexicographic test, then sorted insertion with early exit
+      const std::uint32_t pid = s_ids[w][p];
       if (d2 < kd || pid < kid) {
         int j = K - 1;
         while (j > 0) {
@@ -203,10 +224,10 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
           // each lane scans all points against its own query,
           // two independent distance chains per iteration (fp64 latency)
           for (std::uint32_t p = 0; p < c; p += 2) {
-            const double da = leaf_d2<D>(q, s_pts[w], p);
-            const double db = leaf_d2<D>(q, s_pts[w], p + 1);
-            offer(da, s_ids[w][p]);
-            offer(db, s_ids[w][p + 1]);
+            double da, db;
+            leaf_d2_pair<D>(q, s_pts[w], p, da, db);
+            offer(da, p);
+            offer(db, p + 1);
           }
         } else if (m > 0) {
           // high D, few lanes need this leaf: spread the m x c needed (query, point) pairs
@@ -239,7 +260,7 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
               const int ob = __shfl_sync(0xffffffffu, own, b);
               const double db = __shfl_sync(0xffffffffu, d2, b);
               const std::uint32_t pb = __shfl_sync(0xffffffffu, pp, b);
-              if (lane == ob) offer(db, s_ids[w][pb]);
+              if (lane == ob) offer(db, pb);
             }
             __syncwarp();
             pp += dp;
