@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
       for (int s = 1; s >= 0; --s) {
         bool in = true;
 #pragma unroll
-        for (int j = 0; j < D; ++j) in = in && (pf_hi[j] >= nd.lo[s][j]) && (pf_lo[j] <= nd.hi[s][j]);
+        for (int j = 0; j < D; ++j) in = in && (pf_hi[j] >= nd.lo[j][s]) && (pf_lo[j] <= nd.hi[j][s]);
         if (in && sp < kStack) stk[sp++] = nd.ref[s];
       }
     }

@@ -584,8 +584,8 @@ __global__ void k_emit(const BuildArgs a, std::uint32_t N, const std::uint32_t* 
       const std::uint32_t ch = cb + s;
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        t.lo[s][j] = __double2float_rd(na.lo[static_cast<std::uint64_t>(ch) * D + j]);
-        t.hi[s][j] = __double2float_ru(na.hi[static_cast<std::uint64_t>(ch) * D + j]);
+        t.lo[j][s] = __double2float_rd(na.lo[static_cast<std::uint64_t>(ch) * D + j]);
+        t.hi[j][s] = __double2float_ru(na.hi[static_cast<std::uint64_t>(ch) * D + j]);
       }
       t.ref[s] = (na.flags[ch] & F_LEAF) ? make_leaf_ref(na.start[ch], na.count[ch])
                                          : static_cast<std::uint64_t>(irank_by_slot[na.pos[ch]]);
@@ -652,8 +652,8 @@ __global__ void k_relink(std::uint32_t N, gk_canon_node* canon, TNode<D>* tn, co
     const gk_canon_node& c = canon[ch[s]];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      t.lo[s][j] = __double2float_rd(c.lo[j]);
-      t.hi[s][j] = __double2float_ru(c.hi[j]);
+      t.lo[j][s] = __double2float_rd(c.lo[j]);
+      t.hi[j][s] = __double2float_ru(c.hi[j]);
     }
     t.ref[s] = c.kind == 1 ? make_leaf_ref(c.start, c.count) : static_cast<std::uint64_t>(irank[ch[s]]);
   }

@@ -32,13 +32,14 @@ struct Error : std::runtime_error {
 
 // Traversal node (query-optimised mirror of one internal canonical node):
 // both children's boxes, rounded outward to fp32 (conservative, so pruning
-// stays exact), and the two child references.  A child reference is either an
+// stays exact), interleaved per dimension (lo[j] = {child0, child1}) so one
+// packed f32x2 instruction tests both children, and the two child references.  A child reference is either an
 // internal-node index (rank among internal nodes in vEB order) or, with bit 63
 // set, a leaf: bits [8,56) = first point, bits [0,8) = point count.
 template <int D>
 struct alignas(16) TNode {
-  float lo[2][D];
-  float hi[2][D];
+  float lo[D][2];
+  float hi[D][2];
   std::uint64_t ref[2];
 };
 

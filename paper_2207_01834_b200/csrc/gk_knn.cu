@@ -111,6 +111,50 @@ __device__ __forceinline__ void leaf_d2_pair(const double (&q)[D], const double*
   }
 }
 
+// packed fp32x2 helpers (sm_100: FADD2/FMUL2 with directed rounding)
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  return (static_cast<unsigned long long>(__float_as_uint(b)) << 32) | __float_as_uint(a);
+}
+__device__ __forceinline__ float lo_of(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v)); }
+__device__ __forceinline__ float hi_of(unsigned long long v) { return __uint_as_float(static_cast<unsigned>(v >> 32)); }
+__device__ __forceinline__ unsigned long long sub_rm2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul_rm2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add_rm2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// box_lb for both children of a traversal node at once (same bound, same rounding,
+// two lanes of each packed instruction = the two children)
+template <int D>
+__device__ __forceinline__ void box_lb_pair(const unsigned long long (&qlo2)[D], const unsigned long long (&qhi2)[D],
+                                            const unsigned long long* lo2, const unsigned long long* hi2, float& m0,
+                                            float& m1) {
+  unsigned long long s = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const unsigned long long a = sub_rm2(lo2[j], qhi2[j]);  // lo - q (rounded down)
+    const unsigned long long b = sub_rm2(qlo2[j], hi2[j]);  // q - hi (rounded down)
+    const float t0 = fmaxf(fmaxf(lo_of(a), lo_of(b)), 0.f);
+    const float t1 = fmaxf(fmaxf(hi_of(a), hi_of(b)), 0.f);
+    const unsigned long long t = pk2(t0, t1);
+    const unsigned long long sq = mul_rm2(t, t);
+    s = (j == 0) ? sq : add_rm2(s, sq);
+  }
+  s = mul_rm2(s, pk2(0x1.fffffcp-1f, 0x1.fffffcp-1f));
+  m0 = lo_of(s);
+  m1 = hi_of(s);
+}
+
 template <int D, int K, bool COUNT>
 __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
@@ -158,10 +202,13 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
 #pragma unroll
     for (int j = 0; j < D; ++j) q[j] = 0.0;
   }
+  unsigned long long qlo2[D], qhi2[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     qlo[j] = __double2float_rd(q[j]);
     qhi[j] = __double2float_ru(q[j]);
+    qlo2[j] = pk2(qlo[j], qlo[j]);
+    qhi2[j] = pk2(qhi[j], qhi[j]);
     if (kPairMode) s_q[w][j * 32 + lane] = q[j];
   }
 #pragma unroll
@@ -274,26 +321,21 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
         }
       } else {
         const float4* nd = nodes + ref * (D + 1);
-        float lo0[D], lo1[D], hi0[D], hi1[D];
-        {
-          float f[4 * D];
+        // whole node in D+1 16-byte loads: D (lo0,lo1) pairs, D (hi0,hi1) pairs, 2 child refs
+        unsigned long long u[2 * (D + 1)];
 #pragma unroll
-          for (int v = 0; v < D; ++v) {
-            const float4 x = nd[v];
-            f[4 * v] = x.x; f[4 * v + 1] = x.y; f[4 * v + 2] = x.z; f[4 * v + 3] = x.w;
-          }
-#pragma unroll
-          for (int j = 0; j < D; ++j) {
-            lo0[j] = f[j]; lo1[j] = f[D + j]; hi0[j] = f[2 * D + j]; hi1[j] = f[3 * D + j];
-          }
+        for (int v = 0; v <= D; ++v) {
+          const ulonglong2 x = reinterpret_cast<const ulonglong2*>(nd)[v];
+          u[2 * v] = x.x;
+          u[2 * v + 1] = x.y;
         }
-        const ulonglong2 rr = *reinterpret_cast<const ulonglong2*>(nd + D);
+        const ulonglong2 rr = make_ulonglong2(u[2 * D], u[2 * D + 1]);
         if (COUNT) {
           if (need) c_nodes++;
           c_wn++;
         }
-        const float m0 = box_lb<D>(qlo, qhi, lo0, hi0);
-        const float m1 = box_lb<D>(qlo, qhi, lo1, hi1);
+        float m0, m1;
+        box_lb_pair<D>(qlo2, qhi2, u, u + D, m0, m1);
         const bool w0 = m0 <= kthf, w1 = m1 <= kthf;
         const unsigned b0 = __ballot_sync(0xffffffffu, w0), b1 = __ballot_sync(0xffffffffu, w1);
         if (b0 && b1) {
