@@ -19,7 +19,7 @@
 // records hold both children's fp32 outward-rounded boxes, so one broadcast
 // 64 B load (3D) decides both children.  A leaf's points are staged once per
 // warp into shared memory with coalesced SoA fp64 loads and every lane scans
-// them against its own query; candidates stay sorted in registers.  All trees
+// them against its own query; candidates live in a per-lane max-heap.  All trees
 // of the log structure are walked inside the same kernel, so no per-tree
 // state ever round-trips through HBM.
 #include <cub/cub.cuh>
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
   constexpr int kPairLanes = 10;      // <= this many needing lanes: pair-parallel leaf scan
   __shared__ double s_q[kWarps][kPairMode ? D * 32 : 1];       // the tile's queries, [D][lane]
   __shared__ std::uint8_t s_own[kWarps][32];                   // lanes needing the current leaf
-  // per-lane sorted top-K, one column per thread (conflict-free): [K][blockDim] d2, then [K][blockDim] ids
+  // per-lane top-K heap, one column per thread (conflict-free): [K][blockDim] d2, then [K][blockDim] ids
   extern __shared__ double s_cand[];
   double* cdv = s_cand + threadIdx.x;
   std::uint32_t* civ = reinterpret_cast<std::uint32_t*>(s_cand + K * kWarps * 32) + threadIdx.x;
@@ -216,29 +216,43 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
     cdv[j * CS] = kInf;  // (+inf, kNoPoint): KnnBuffer's initial bound
     civ[j * CS] = GK_NO_POINT;
   }
-  double kd = kInf;                 // current k-th (d2, id)
+  double kd = kInf;                 // current k-th (d2, id) = heap root
   std::uint32_t kid = GK_NO_POINT;
   // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
   float kthf = active ? __int_as_float(0x7f800000) : -1.f;
 
   // offer staged leaf point p (distance d2) to this lane's k-buffer
+  // The k-buffer is a max-heap on (d2, id) in this lane's shared-memory column: the root
+  // is the current k-th entry, an accepted point replaces it and sifts down (<= log2 K
+  // levels, so the warp's divergent inserts cost little); sorted once at the end.
+  auto sift_down = [&](double x, std::uint32_t xid, int n) {
+    int i = 0;
+    while (true) {
+      int c = 2 * i + 1;
+      if (c >= n) break;
+      double cv = cdv[c * CS];
+      std::uint32_t cid = civ[c * CS];
+      if (c + 1 < n) {
+        const double rv = cdv[(c + 1) * CS];
+        const std::uint32_t rid = civ[(c + 1) * CS];
+        if (lexlt(cv, cid, rv, rid)) { ++c; cv = rv; cid = rid; }
+      }
+      if (!lexlt(x, xid, cv, cid)) break;
+      cdv[i * CS] = cv;
+      civ[i * CS] = cid;
+      i = c;
+    }
+    cdv[i * CS] = x;
+    civ[i * CS] = xid;
+  };
+  // offer staged leaf point p (distance d2) to this lane's k-buffer
   auto offer = [&](double d2, std::uint32_t p) {
-    if (d2 <= kd) {  // rare: lexicographic test, then sorted insertion with early exit
+    if (d2 <= kd) {  // rare: lexicographic test against the k-th, then heap replace
       const std::uint32_t pid = s_ids[w][p];
       if (d2 < kd || pid < kid) {
-        int j = K - 1;
-        while (j > 0) {
-          const double cv = cdv[(j - 1) * CS];
-          const std::uint32_t cid = civ[(j - 1) * CS];
-          if (!lexlt(d2, pid, cv, cid)) break;
-          cdv[j * CS] = cv;
-          civ[j * CS] = cid;
-          --j;
-        }
-        cdv[j * CS] = d2;
-        civ[j * CS] = pid;
-        kd = cdv[(K - 1) * CS];
-        kid = civ[(K - 1) * CS];
+        sift_down(d2, pid, K);
+        kd = cdv[0];
+        kid = civ[0];
         kthf = __double2float_ru(kd);
       }
     }
@@ -298,7 +312,7 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
                 const double tt = __dsub_rn(qo[j * 32], s_pts[w][j * GK_MAX_LEAF + pp]);
                 d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
               }
-              cand = d2 <= s_cand[(K - 1) * CS + w * 32 + own];
+              cand = d2 <= s_cand[w * 32 + own];  // owner's heap root = its k-th distance
             }
             unsigned bal = __ballot_sync(0xffffffffu, cand);
             while (bal) {
@@ -380,6 +394,16 @@ __global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(c
   }
 
   if (active) {
+    // heapsort: pop the max into position n-1 (KnnBuffer::extract order, ascending (d2, id))
+    for (int n = K - 1; n > 0; --n) {
+      const double top = cdv[0];
+      const std::uint32_t topid = civ[0];
+      const double last = cdv[n * CS];
+      const std::uint32_t lastid = civ[n * CS];
+      cdv[n * CS] = top;
+      civ[n * CS] = topid;
+      sift_down(last, lastid, n);
+    }
 #pragma unroll
     for (int j = 0; j < K; ++j)
       if (j < k) {
