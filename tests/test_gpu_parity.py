@@ -300,3 +300,41 @@ def test_bloom_filter(gk):
     g2 = gk.BDLTree(3, X=4)
     g2.insert(np.array([[0.0, -0.0, 1.0]] * 4))
     assert g2.bloom_may_contain(0, np.array([[-0.0, 0.0, 1.0]])).all()  # -0 == +0 probes the same bits
+
+
+def _sampled_script_parity(gk, oracle, cfg, nsample=20000, trees=True):
+    """Full-size BASELINE script on both sides: structure (F, buffer, live counts, every static tree's
+    permutation/tombstones/nodes) bit-exact after every operation, kNN rows exact on a seeded sample."""
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(cfg)
+    g = gk.BDLTree(d)
+    o = oracle.BDLTree(d)
+    rng = np.random.default_rng(cfg)
+    for step, op in enumerate(script):
+        if op[0] == "insert":
+            g.insert(op[1]); o.insert(op[1])
+            assert_struct_equal(g, o, trees)
+        elif op[0] == "erase":
+            assert g.erase(op[1]) == o.erase(op[1])
+            assert_struct_equal(g, o, trees)
+        else:
+            Q, k = op[1], op[2]
+            ids, d2 = g.knn(Q, k)
+            rows = np.sort(rng.choice(len(Q), min(nsample, len(Q)), replace=False))
+            assert_knn_equal((ids[rows], d2[rows]), o.knn(Q[rows], k), f"config {cfg} step {step}")
+            assert (np.diff(d2, axis=1) >= 0).all()
+
+
+@pytest.mark.slow
+def test_full_c3_sampled(gk, oracle):
+    _sampled_script_parity(gk, oracle, 3)
+
+
+@pytest.mark.slow
+def test_full_c4_sampled(gk, oracle):
+    _sampled_script_parity(gk, oracle, 4, nsample=5000)
+
+
+@pytest.mark.slow
+def test_full_c5_sampled(gk, oracle):
+    _sampled_script_parity(gk, oracle, 5)
