@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libgkbdl.so")
+# GK_LIB overrides the library path (A/B experiments between two builds of the same ABI)
+LIB_PATH = os.environ.get("GK_LIB") or os.path.join(HERE, "_lib", "libgkbdl.so")
 
 NO_POINT = 0xFFFFFFFF  # geokit::core::kNoPoint
 MAX_K = 32
