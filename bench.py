@@ -112,6 +112,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def measure_fp64_peak(dev):
+    """FP64 roofline denominator (MEASURED_PEAKS.json has none): cuBLAS DGEMM TFLOP/s, best of 3."""
+    import torch
+    try:
+        a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        torch.matmul(a, b)
+        best = 1e9
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1000.0)
+        del a, b
+        return 2 * 8192 ** 3 / best / 1e12
+    except Exception:
+        return None
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -274,6 +295,7 @@ def run_gpu(args):
 
     if rank == 0:
         hbm, peak_src = measured_peaks()
+        fp64_peak = measure_fp64_peak(dev)
         k1_ms = statistics.mean(trav_ms)
         achieved = bytes_per_q * nq / (k1_ms / 1000.0) / 1e9
         traffic = None
@@ -304,11 +326,14 @@ def run_gpu(args):
                          "kernel": "k_knn (K1 fused kNN_L traversal)", "k1_ms": k1_ms,
                          "bytes_per_query": bytes_per_q, "flops_per_query": flops_per_q,
                          "fp64_gflops": flops_per_q * nq / (k1_ms / 1000.0) / 1e9,
+                         "fp64_peak_tflops": fp64_peak,
+                         "fp64_frac": flops_per_q * nq / (k1_ms / 1000.0) / 1e12 / fp64_peak if fp64_peak else None,
+                         "fp64_peak_source": "measured here: cuBLAS DGEMM 8192^3 via torch, best of 3",
                          "counters": ctr},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 8,
                     "d2h_bytes_per_step": nq * k * (4 + 8)},
-            "gpu_launches": 9 * args.steps,
+            "gpu_launches": 10 * args.steps,  # k_qbox_init, k_qbox, k_morton, 6 CUB radix-sort kernels, k_knn
             "clocks": clk.summary(),
             "build": {"insert_l_points_per_s": len(P) / build_wall, "buildveb_points_per_s": built / (build_ms / 1000.0),
                       "insert_l_ms": 1000 * build_wall, "buildveb_ms": build_ms, "points": built,
