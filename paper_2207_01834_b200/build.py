@@ -16,6 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libgkbdl.so")
+CLI = os.path.join(OUT_DIR, "gk_bdl_cli")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 CU_SOURCES = ["gk_build.cu", "gk_knn.cu", "gk_bdl.cu"]
@@ -78,6 +79,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if force or jobs or _stale(LIB, objs):
         cmd = [_nvcc(), "-shared", "-ccbin", _cxx(), "-o", LIB, *objs, "-Xcompiler", "-fopenmp", "-lgomp"]
         run(cmd)
+    cli_src = os.path.join(CSRC, "gk_bdl_cli.cpp")
+    if force or _stale(CLI, [cli_src, LIB] + headers):  # the CLI harness over the C ABI
+        run([_cxx(), "-O2", "-std=c++17", "-ffp-contract=off", cli_src, "-o", CLI, "-L", OUT_DIR, "-lgkbdl",
+             "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

@@ -57,3 +57,12 @@ def _compile_client(out):
 def test_cpp_binding_compiles(gk, tmp_path):
     """include/geokit_bdl.hpp (the reference-side C++ binding) compiles and links against the ABI"""
     _compile_client(str(tmp_path / "client"))
+
+
+def test_cli_usage_without_gpu(gk):
+    """the CLI harness is built and rejects bad usage with exit code 1"""
+    import subprocess
+    exe = os.path.join(ROOT, "paper_2207_01834_b200", "_lib", "gk_bdl_cli")
+    assert os.path.exists(exe)
+    assert subprocess.run([exe], capture_output=True).returncode == 1
+    assert subprocess.run([exe, "frobnicate"], capture_output=True).returncode == 1
