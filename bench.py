@@ -308,7 +308,7 @@ def run_gpu(args):
             except Exception:
                 traffic = None
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is reported at N=1 only
             o, threads, build_s, m = cpu_knn_rate(P, Q, k, d, args.cpu_seconds, sample_cap=len(Q))
             t0 = time.perf_counter()
             o.knn(Q[:m], k)
