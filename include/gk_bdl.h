@@ -47,7 +47,7 @@ enum gk_status {
 
 enum gk_heuristic { GK_SPATIAL_MEDIAN = 0, GK_OBJECT_MEDIAN = 1 }; /* PAPER.md:1484-1487 */
 
-#define GK_MAX_K 32
+#define GK_MAX_K 256
 #define GK_MAX_LEAF 32
 
 typedef struct gk_bdl gk_bdl; /* opaque handle: owns all device arenas + one CUDA stream */
@@ -101,7 +101,7 @@ int gk_bdl_insert_device(gk_bdl* h, const double* pts_dev, uint64_t n);
 int gk_bdl_erase(gk_bdl* h, const double* pts, uint64_t n, uint64_t* n_erased);
 int gk_bdl_erase_device(gk_bdl* h, const double* pts_dev, uint64_t n, uint64_t* n_erased);
 
-/* kNN_L: exact k nearest live points of every query, 1 <= k <= GK_MAX_K. */
+/* kNN_L: exact k nearest live points of every query, 1 <= k <= GK_MAX_K (256). */
 int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, double* d2);
 int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev);
 /* Instrumented kNN_L (same results) that also counts the work of §8(d). */

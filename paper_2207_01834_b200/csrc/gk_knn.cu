@@ -34,62 +34,13 @@ namespace gk {
 namespace {
 
 // warps per block: 8, or 4 for K > 16 so the shared-memory k-buffers (12 B x K per lane) still
-// leave room for several blocks per SM
+// leave room for several blocks per SM; K = 0 is the runtime-k instantiation (32 < k <= 256)
 template <int K>
-__host__ __device__ constexpr int warps_for() { return K > 16 ? 4 : 8; }
+__host__ __device__ constexpr int warps_for() { return K == 0 ? 2 : (K > 16 ? 4 : 8); }
+constexpr int kMaxRuntimeK = 256;
 
 __device__ __forceinline__ bool lexlt(double a, std::uint32_t ia, double b, std::uint32_t ib) {
   return a < b || (a == b && ia < ib);
-}
-
-// Sorted insertion of (x, id) into the register top-K (x is known to beat slot K-1).
-// Slot j takes slot j-1 when x precedes it, x itself when x precedes slot j but
-// not slot j-1, else keeps its value; each comparison is made once.
-template <int K>
-__device__ __forceinline__ void insert_cand(double x, std::uint32_t id, double (&cd)[K], std::uint32_t (&ci)[K]) {
-  bool after = true;  // x precedes the (old) value of slot j
-#pragma unroll
-  for (int j = K - 1; j > 0; --j) {
-    const bool before = lexlt(x, id, cd[j - 1], ci[j - 1]);
-    const double v = before ? cd[j - 1] : (after ? x : cd[j]);
-    const std::uint32_t vi = before ? ci[j - 1] : (after ? id : ci[j]);
-    cd[j] = v;
-    ci[j] = vi;
-    after = before;
-  }
-  if (after) {
-    cd[0] = x;
-    ci[0] = id;
-  }
-}
-
-// fp32 lower bound of the canonical fp64 d2 of every point inside the box
-// [lo, hi]: per-dimension gaps rounded down from (q rounded out), squares and
-// sums rounded down, then scaled by (1 - 2^-23) rounded down so that it stays
-// below the fp64 rounding of the true d2 (relative error <= (D+1) 2^-53).
-template <int D>
-__device__ __forceinline__ float box_lb(const float (&qlo)[D], const float (&qhi)[D], const float* lo, const float* hi) {
-  const float t0 = fmaxf(fmaxf(__fsub_rd(lo[0], qhi[0]), __fsub_rd(qlo[0], hi[0])), 0.f);
-  float s = __fmul_rd(t0, t0);
-#pragma unroll
-  for (int j = 1; j < D; ++j) {
-    const float t = fmaxf(fmaxf(__fsub_rd(lo[j], qhi[j]), __fsub_rd(qlo[j], hi[j])), 0.f);
-    s = __fadd_rd(s, __fmul_rd(t, t));
-  }
-  return __fmul_rd(s, 0x1.fffffcp-1f);
-}
-
-// distance of the query to staged leaf point p (canonical order, no FMA)
-template <int D>
-__device__ __forceinline__ double leaf_d2(const double (&q)[D], const double* sp, int p) {
-  const double t0 = __dsub_rn(q[0], sp[p]);
-  double d2 = __dmul_rn(t0, t0);  // 0 + t0^2 == t0^2 exactly
-#pragma unroll
-  for (int j = 1; j < D; ++j) {
-    const double tt = __dsub_rn(q[j], sp[j * GK_MAX_LEAF + p]);
-    d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
-  }
-  return d2;
 }
 
 // distances of the query to staged leaf points p and p+1 (p even): one 16-byte shared
@@ -133,8 +84,11 @@ __device__ __forceinline__ unsigned long long add_rm2(unsigned long long a, unsi
   return r;
 }
 
-// box_lb for both children of a traversal node at once (same bound, same rounding,
-// two lanes of each packed instruction = the two children)
+// fp32 lower bound of the canonical fp64 d2 of every point inside each child's box
+// [lo, hi], both children at once (the two halves of each packed f32x2 instruction):
+// per-dimension gaps rounded down from (q rounded out), squares and sums rounded down,
+// then scaled by (1 - 2^-23) rounded down so that the bound stays below the fp64
+// rounding of the true d2 (relative error <= (D+1) 2^-53).
 template <int D>
 __device__ __forceinline__ void box_lb_pair(const unsigned long long (&qlo2)[D], const unsigned long long (&qhi2)[D],
                                             const unsigned long long* lo2, const unsigned long long* hi2, float& m0,
@@ -155,13 +109,14 @@ __device__ __forceinline__ void box_lb_pair(const unsigned long long (&qlo2)[D],
   m1 = hi_of(s);
 }
 
-template <int D, int K, bool COUNT>
-__global__ void __launch_bounds__(warps_for<K>() * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
+template <int D, int KT, bool COUNT>
+__global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(const TreeSet ts, const double* __restrict__ Q,
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
                                                         unsigned long long* __restrict__ counters,
                                                         unsigned* __restrict__ tile_ctr) {
-  constexpr int kWarps = warps_for<K>();
+  constexpr int kWarps = warps_for<KT>();
+  const int K = KT > 0 ? KT : k;  // k-buffer size (compile-time for the common k)
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ __align__(16) double s_pts[kWarps][D * GK_MAX_LEAF];
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
@@ -490,29 +445,32 @@ __global__ void k_morton(const double* __restrict__ Q, std::uint64_t nq, const u
   idx[i] = static_cast<std::uint32_t>(i);
 }
 
-template <int D, int K>
+template <int D, int KT>
 void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, int k, std::uint32_t* ids,
               double* d2, unsigned long long* ctr, cudaStream_t st) {
-  constexpr int kWarps = warps_for<K>();
+  constexpr int kWarps = warps_for<KT>();
   const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
-  const int smem = K * kWarps * 32 * 12;  // per-lane top-K columns
+  const int smem = (KT > 0 ? KT : k) * kWarps * 32 * 12;        // per-lane top-K columns
+  const int smem_max = (KT > 0 ? KT : kMaxRuntimeK) * kWarps * 32 * 12;
   static std::once_flag once;             // per (D, K) instantiation
-  static int resident = 0;                // co-resident blocks at this smem size
+  static int sm_count = 0;
   std::call_once(once, [&] {
-    GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    GK_CUDA(cudaFuncSetAttribute(k_knn<D, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int dev = 0, sms = 0, per = 0;
+    GK_CUDA(cudaFuncSetAttribute(k_knn<D, KT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    GK_CUDA(cudaFuncSetAttribute(k_knn<D, KT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    int dev = 0, sms = 0;
     GK_CUDA(cudaGetDevice(&dev));
     GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn<D, K, false>, kWarps * 32, smem));
-    resident = std::max(1, per) * sms;
+    sm_count = sms;
   });
+  int per = 0;  // resident blocks at this launch's shared-memory size
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn<D, KT, false>, kWarps * 32, smem));
+  const int resident = std::max(1, per) * sm_count;
   const unsigned grid = std::min<unsigned>(blocks, static_cast<unsigned>(resident));
   unsigned* tile_ctr = nullptr;
   GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
   GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
-  if (ctr) k_knn<D, K, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
-  else k_knn<D, K, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
+  if (ctr) k_knn<D, KT, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
+  else k_knn<D, KT, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
   GK_CUDA(cudaFreeAsync(tile_ctr, st));
 }
 
@@ -526,7 +484,8 @@ void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* pe
   else if (k <= 8) launch_k<D, 8>(ts, Q, perm, nq, k, ids, d2, ctr, st);
   else if (k <= 10) launch_k<D, 10>(ts, Q, perm, nq, k, ids, d2, ctr, st);
   else if (k <= 16) launch_k<D, 16>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= 32) launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st);
 }
 
 template <int D>

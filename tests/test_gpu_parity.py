@@ -108,7 +108,7 @@ def test_golden_veb_layout(gk, oracle):  # SPEC.md:476 / Fig. vebconstruct, thro
 
 
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
-@pytest.mark.parametrize("k", [1, 3, 10, 16, 32])
+@pytest.mark.parametrize("k", [1, 3, 10, 16, 32, 33, 100, 256])
 def test_dims_and_k(gk, oracle, d, k):
     rng = np.random.default_rng(100 * d + k)
     P = rng.random((6000, d))
@@ -154,7 +154,7 @@ def test_empty_and_short(gk, oracle):
 def test_errors(gk):
     g = gk.BDLTree(3)
     with pytest.raises(NotImplementedError):
-        g.knn(np.zeros((1, 3)), 33)
+        g.knn(np.zeros((1, 3)), 257)
     with pytest.raises(ValueError):
         g.knn(np.zeros((1, 3)), 0)
     with pytest.raises(ValueError):
