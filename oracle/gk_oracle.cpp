@@ -20,8 +20,10 @@
 // every ambiguity is frozen here and listed in DESIGN.md "Frozen decisions".
 //
 // Parity pins: KnnBuf and Rng are checked bit-for-bit against the reference's
-// own headers compiled into oracle/_ref (tests/test_oracle_pins.py); the tree
-// algorithms are pinned by the SPEC known-answer examples (tests/test_oracle.py).
+// own headers compiled into oracle/_ref (tests/test_oracle_pins.py).  The tree
+// algorithms have no reference implementation to run: they are
+// pinned only by the SPEC known-answer examples and an exact brute-force scan
+// (tests/test_oracle.py) — beyond those, tree-level parity is unpinned.
 // Floating point: compile with -ffp-contract=off; squared distance is
 // sum_{j=0..D-1} (q_j - p_j)^2 accumulated left-to-right, no FMA.
 
