@@ -85,6 +85,7 @@ typedef struct gk_knn_counters {
   uint64_t dists;        /* distance evaluations needed */
   uint64_t warp_nodes;   /* node loads actually issued (one per warp tile) */
   uint64_t warp_leaves;  /* leaf loads actually issued (one per warp tile) */
+  uint64_t inserts;      /* points accepted into a k-buffer (all queries) */
 } gk_knn_counters;
 
 const char* gk_last_error(void);

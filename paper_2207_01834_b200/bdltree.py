@@ -46,7 +46,7 @@ class _Info(C.Structure):
 class KnnCounters(C.Structure):
     _fields_ = [("node_bytes", C.c_uint64), ("leaf_bytes", C.c_uint64), ("nodes", C.c_uint64),
                 ("leaves", C.c_uint64), ("dists", C.c_uint64), ("warp_nodes", C.c_uint64),
-                ("warp_leaves", C.c_uint64)]
+                ("warp_leaves", C.c_uint64), ("inserts", C.c_uint64)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}

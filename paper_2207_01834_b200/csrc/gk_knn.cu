@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   const int w = threadIdx.x >> 5;
   const unsigned ntiles = static_cast<unsigned>((nq + 31) / 32);
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0;
+  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0, c_ins = 0;
   float mdst[kStack];
 
   // persistent warps: each grabs the next 32-query tile (Morton order keeps
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
         kd = cdv[0];
         kid = civ[0];
         kthf = __double2float_ru(kd);
+        if (COUNT) c_ins++;
       }
     }
   };
@@ -370,9 +371,9 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
 
   if (COUNT) {
     const unsigned long long node_b = sizeof(TNode<D>), pt_b = 8 * D + 4;
-    unsigned long long v[3] = {c_nodes, c_leaves, c_dists};
+    unsigned long long v[4] = {c_nodes, c_leaves, c_dists, c_ins};
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
     if (lane == 0) {
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
       atomicAdd(&counters[4], v[2]);
       atomicAdd(&counters[5], c_wn);
       atomicAdd(&counters[6], c_wl);
+      atomicAdd(&counters[7], v[3]);
     }
   }
 }
@@ -551,6 +553,7 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
     counters->dists = h[4];
     counters->warp_nodes = h[5];
     counters->warp_leaves = h[6];
+    counters->inserts = h[7];
     GK_CUDA(cudaFreeAsync(ctr, st));
   }
   GK_CUDA(cudaFreeAsync(perm, st));
