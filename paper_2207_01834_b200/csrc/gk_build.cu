@@ -101,6 +101,10 @@ __device__ __forceinline__ std::uint32_t block_sum(std::uint32_t v, std::uint32_
 }
 
 __device__ __forceinline__ void sync_all(cg::grid_group& grid) {
+  if (gridDim.x == 1) {  // small trees build in one block: a block barrier is enough
+    __syncthreads();
+    return;
+  }
   grid.sync();
   __threadfence();  // gpu-scope fence: also invalidates this SM's L1 (CCTL.IVALL)
 }
