@@ -338,3 +338,25 @@ def test_full_c4_sampled(gk, oracle):
 @pytest.mark.slow
 def test_full_c5_sampled(gk, oracle):
     _sampled_script_parity(gk, oracle, 5)
+
+
+@pytest.mark.slow
+def test_object_median_at_scale(gk, oracle):
+    """object-median heuristic on 1M points: every level runs the device radix select
+    (thousands of object nodes per level, batched); permutation + nodes bit-exact"""
+    rng = np.random.default_rng(21)
+    P = rng.random((1_000_000, 3))
+    Q = rng.random((20000, 3))
+    run_script(gk, oracle, 3, [("insert", P), ("knn", Q, 10)], X=1_000_000, heur=1)
+
+
+@pytest.mark.slow
+def test_heavy_duplicates_at_scale(gk, oracle):
+    """600k points on 2000 distinct sites: degenerate spatial splits everywhere -> large
+    object-median fallbacks keyed by (x_c, id); then erase whole sites (all duplicates)"""
+    rng = np.random.default_rng(22)
+    sites = rng.random((2000, 2))
+    P = sites[rng.integers(0, 2000, 600_000)]
+    script = [("insert", P), ("knn", sites[:500], 16), ("erase", sites[:300]), ("knn", sites[:500], 16),
+              ("insert", P[:5000]), ("knn", rng.random((2000, 2)), 7)]
+    run_script(gk, oracle, 2, script, X=4096)
