@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--config", type=int, default=2)
@@ -86,6 +86,13 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
+
+    def wait_started(self, timeout: float = 3.0):
+        """block until nvidia-smi delivers its first sample, so the timed region is covered"""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        self.rows.clear()
 
     def __exit__(self, *a):
         if self.proc:
@@ -261,6 +268,7 @@ def run_gpu(args):
     torch.cuda.synchronize(dev)
     step_ms, trav_ms = [], []
     with ClockSampler(dev.index) as clk:
+        clk.wait_started()
         for _ in range(args.steps):
             flush.fill_(1.0)
             torch.cuda.synchronize(dev)
