@@ -38,6 +38,7 @@ namespace {
 template <int K>
 __host__ __device__ constexpr int warps_for() { return K == 0 ? 2 : (K > 16 ? 4 : 8); }
 constexpr int kMaxRuntimeK = 256;
+constexpr bool kHilbertOrder = true;  // K2 key: Hilbert (true) or Morton (false)
 
 __device__ __forceinline__ bool lexlt(double a, std::uint32_t ia, double b, std::uint32_t ib) {
   return a < b || (a == b && ia < ib);
@@ -437,6 +438,32 @@ __global__ void k_morton(const double* __restrict__ Q, std::uint64_t nq, const u
     int c = static_cast<int>(f * static_cast<double>(1u << B));
     c = c < 0 ? 0 : (c > static_cast<int>((1u << B) - 1) ? static_cast<int>((1u << B) - 1) : c);
     cell[j] = static_cast<std::uint32_t>(c);
+  }
+  if (kHilbertOrder) {
+    // Hilbert index (Skilling's transpose form: undo excess work, then Gray-encode),
+    // fewer jumps than Morton between consecutive keys -> more compact 32-query tiles
+#pragma unroll
+    for (std::uint32_t Qb = 1u << (B - 1); Qb > 1; Qb >>= 1) {
+      const std::uint32_t P = Qb - 1;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        if (cell[j] & Qb) {
+          cell[0] ^= P;
+        } else {
+          const std::uint32_t t = (cell[0] ^ cell[j]) & P;
+          cell[0] ^= t;
+          cell[j] ^= t;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 1; j < D; ++j) cell[j] ^= cell[j - 1];
+    std::uint32_t t = 0;
+#pragma unroll
+    for (std::uint32_t Qb = 1u << (B - 1); Qb > 1; Qb >>= 1)
+      if (cell[D - 1] & Qb) t ^= Qb - 1;
+#pragma unroll
+    for (int j = 0; j < D; ++j) cell[j] ^= t;
   }
   std::uint32_t key = 0;
 #pragma unroll
