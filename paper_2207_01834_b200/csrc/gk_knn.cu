@@ -25,7 +25,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "gk_common.cuh"
@@ -517,8 +519,44 @@ void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* pe
   else launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st);
 }
 
+// K2 key for D >= 5: the leaf-order position of the query's leaf in the largest tree.
+// At high D a 32-bit space-filling key has too few bits per dimension (4 in 7D) to
+// separate clustered data; the kd-tree's own leaf order adapts to the density
+// (C3: +55 % over the 7D Hilbert key; at D <= 4 Hilbert is better: C2 -20 % with kd).
 template <int D>
-void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, cudaStream_t st) {
+__global__ void k_kdkey(const double* __restrict__ Q, std::uint64_t nq, const TreeRef t0, std::uint32_t* keys,
+                        std::uint32_t* idx) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nq) return;
+  unsigned long long qlo2[D], qhi2[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double x = Q[i * D + j];
+    const float lo = __double2float_rd(x), hi = __double2float_ru(x);
+    qlo2[j] = pk2(lo, lo);
+    qhi2[j] = pk2(hi, hi);
+  }
+  std::uint64_t ref = t0.root;
+  const float4* nodes = static_cast<const float4*>(t0.tnodes);
+  while (!is_leaf_ref(ref)) {
+    const float4* nd = nodes + ref * (D + 1);
+    unsigned long long u[2 * (D + 1)];
+#pragma unroll
+    for (int v = 0; v <= D; ++v) {
+      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(nd)[v];
+      u[2 * v] = x.x;
+      u[2 * v + 1] = x.y;
+    }
+    float m0, m1;
+    box_lb_pair<D>(qlo2, qhi2, u, u + D, m0, m1);
+    ref = (m1 < m0) ? u[2 * D + 1] : u[2 * D];
+  }
+  keys[i] = static_cast<std::uint32_t>(leaf_start(ref));
+  idx[i] = static_cast<std::uint32_t>(i);
+}
+
+template <int D>
+void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, cudaStream_t st, const TreeRef* t0) {
   unsigned long long* box = nullptr;
   std::uint32_t *keys = nullptr, *keys2 = nullptr, *idx = nullptr;
   GK_CUDA(cudaMallocAsync(&box, 2 * D * sizeof(unsigned long long), st));
@@ -528,11 +566,16 @@ void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, c
   k_qbox_init<<<1, 32, 0, st>>>(box, D);
   const unsigned gb = static_cast<unsigned>(std::min<std::uint64_t>((nq + 255) / 256, 148 * 8));
   k_qbox<D><<<gb, 256, 0, st>>>(Q, nq, box);
-  k_morton<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, box, keys, idx);
+  int bits = (32 / D) * D;
+  if (D >= 5 && t0) {
+    k_kdkey<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, *t0, keys, idx);
+    bits = 32;
+  } else {
+    k_morton<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, box, keys, idx);
+  }
   GK_CHECK_LAUNCH();
   void* tmp = nullptr;
   std::size_t tb = 0;
-  const int bits = (32 / D) * D;
   GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, perm_out, static_cast<int>(nq), 0, bits, st));
   GK_CUDA(cudaMallocAsync(&tmp, tb, st));
   GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, perm_out, static_cast<int>(nq), 0, bits, st));
@@ -559,7 +602,7 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
   switch (d) {
 #define GK_D(DD)                                                   \
   case DD:                                                         \
-    order_queries<DD>(q_dev, nq, perm, st);                        \
+    order_queries<DD>(q_dev, nq, perm, st, trees.count > 0 ? &trees.t[0] : nullptr);                        \
     if (ev_k0) GK_CUDA(cudaEventRecord(ev_k0, st));                \
     launch_d<DD>(k, trees, q_dev, perm, nq, ids_dev, d2_dev, ctr, st); \
     if (ev_k1) GK_CUDA(cudaEventRecord(ev_k1, st));                \
