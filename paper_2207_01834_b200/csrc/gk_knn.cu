@@ -179,7 +179,6 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
   float kthf = active ? __int_as_float(0x7f800000) : -1.f;
 
-  // offer staged leaf point p (distance d2) to this lane's k-buffer
   // The k-buffer is a max-heap on (d2, id) in this lane's shared-memory column: the root
   // is the current k-th entry, an accepted point replaces it and sifts down (<= log2 K
   // levels, so the warp's divergent inserts cost little); sorted once at the end.
