@@ -25,9 +25,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
-#include <cstdlib>
 #include <mutex>
-#include <string>
+#include <type_traits>
 #include <vector>
 
 #include "gk_common.cuh"
@@ -424,10 +423,47 @@ __global__ void k_qbox(const double* __restrict__ Q, std::uint64_t nq, unsigned 
     }
 }
 
-template <int D>
-__global__ void k_morton(const double* __restrict__ Q, std::uint64_t nq, const unsigned long long* __restrict__ box,
-                         std::uint32_t* keys, std::uint32_t* idx) {
-  constexpr int B = 32 / D;
+// Hilbert index of a D-dim cell with B bits per dim (Skilling's transpose + Gray code)
+template <int D, int B, class KeyT>
+__device__ __forceinline__ KeyT hilbert_key(std::uint32_t (&cell)[D]) {
+#pragma unroll
+  for (std::uint32_t Qb = 1u << (B - 1); Qb > 1; Qb >>= 1) {
+    const std::uint32_t P = Qb - 1;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if (cell[j] & Qb) {
+        cell[0] ^= P;
+      } else {
+        const std::uint32_t t = (cell[0] ^ cell[j]) & P;
+        cell[0] ^= t;
+        cell[j] ^= t;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 1; j < D; ++j) cell[j] ^= cell[j - 1];
+  std::uint32_t t = 0;
+#pragma unroll
+  for (std::uint32_t Qb = 1u << (B - 1); Qb > 1; Qb >>= 1)
+    if (cell[D - 1] & Qb) t ^= Qb - 1;
+#pragma unroll
+  for (int j = 0; j < D; ++j) cell[j] ^= t;
+  KeyT key = 0;
+#pragma unroll
+  for (int b = B - 1; b >= 0; --b)
+#pragma unroll
+    for (int j = 0; j < D; ++j) key = (key << 1) | ((cell[j] >> b) & 1u);
+  return key;
+}
+
+// space-filling-curve key of each query over the batch's bounding box: Hilbert order
+// (fewer jumps than Morton between consecutive keys -> more compact 32-query packets).
+// 32-bit keys for D <= 4; at D >= 5 they would leave only 4-6 bits per dimension, too
+// coarse for clustered data (C3), so 64-bit keys (9 bits per dimension in 7D) are used.
+template <int D, class Key>
+__global__ void k_curve_key(const double* __restrict__ Q, std::uint64_t nq, const unsigned long long* __restrict__ box,
+                            Key* keys, std::uint32_t* idx) {
+  constexpr int B = (8 * static_cast<int>(sizeof(Key)) - (sizeof(Key) == 8 ? 1 : 0)) / D;
   std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= nq) return;
   std::uint32_t cell[D];
@@ -440,37 +476,15 @@ __global__ void k_morton(const double* __restrict__ Q, std::uint64_t nq, const u
     c = c < 0 ? 0 : (c > static_cast<int>((1u << B) - 1) ? static_cast<int>((1u << B) - 1) : c);
     cell[j] = static_cast<std::uint32_t>(c);
   }
+  Key key = 0;
   if (kHilbertOrder) {
-    // Hilbert index (Skilling's transpose form: undo excess work, then Gray-encode),
-    // fewer jumps than Morton between consecutive keys -> more compact 32-query tiles
+    key = hilbert_key<D, B, Key>(cell);
+  } else {
 #pragma unroll
-    for (std::uint32_t Qb = 1u << (B - 1); Qb > 1; Qb >>= 1) {
-      const std::uint32_t P = Qb - 1;
+    for (int b = B - 1; b >= 0; --b)
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if (cell[j] & Qb) {
-          cell[0] ^= P;
-        } else {
-          const std::uint32_t t = (cell[0] ^ cell[j]) & P;
-          cell[0] ^= t;
-          cell[j] ^= t;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 1; j < D; ++j) cell[j] ^= cell[j - 1];
-    std::uint32_t t = 0;
-#pragma unroll
-    for (std::uint32_t Qb = 1u << (B - 1); Qb > 1; Qb >>= 1)
-      if (cell[D - 1] & Qb) t ^= Qb - 1;
-#pragma unroll
-    for (int j = 0; j < D; ++j) cell[j] ^= t;
+      for (int j = 0; j < D; ++j) key = (key << 1) | ((cell[j] >> b) & 1u);
   }
-  std::uint32_t key = 0;
-#pragma unroll
-  for (int b = B - 1; b >= 0; --b)
-#pragma unroll
-    for (int j = 0; j < D; ++j) key = (key << 1) | ((cell[j] >> b) & 1u);
   keys[i] = key;
   idx[i] = static_cast<std::uint32_t>(i);
 }
@@ -518,60 +532,21 @@ void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* pe
   else launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st);
 }
 
-// K2 key for D >= 5: the leaf-order position of the query's leaf in the largest tree.
-// At high D a 32-bit space-filling key has too few bits per dimension (4 in 7D) to
-// separate clustered data; the kd-tree's own leaf order adapts to the density
-// (C3: +55 % over the 7D Hilbert key; at D <= 4 Hilbert is better: C2 -20 % with kd).
 template <int D>
-__global__ void k_kdkey(const double* __restrict__ Q, std::uint64_t nq, const TreeRef t0, std::uint32_t* keys,
-                        std::uint32_t* idx) {
-  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-  if (i >= nq) return;
-  unsigned long long qlo2[D], qhi2[D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    const double x = Q[i * D + j];
-    const float lo = __double2float_rd(x), hi = __double2float_ru(x);
-    qlo2[j] = pk2(lo, lo);
-    qhi2[j] = pk2(hi, hi);
-  }
-  std::uint64_t ref = t0.root;
-  const float4* nodes = static_cast<const float4*>(t0.tnodes);
-  while (!is_leaf_ref(ref)) {
-    const float4* nd = nodes + ref * (D + 1);
-    unsigned long long u[2 * (D + 1)];
-#pragma unroll
-    for (int v = 0; v <= D; ++v) {
-      const ulonglong2 x = reinterpret_cast<const ulonglong2*>(nd)[v];
-      u[2 * v] = x.x;
-      u[2 * v + 1] = x.y;
-    }
-    float m0, m1;
-    box_lb_pair<D>(qlo2, qhi2, u, u + D, m0, m1);
-    ref = (m1 < m0) ? u[2 * D + 1] : u[2 * D];
-  }
-  keys[i] = static_cast<std::uint32_t>(leaf_start(ref));
-  idx[i] = static_cast<std::uint32_t>(i);
-}
-
-template <int D>
-void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, cudaStream_t st, const TreeRef* t0) {
+void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, cudaStream_t st) {
+  using Key = std::conditional_t<(D >= 5), unsigned long long, std::uint32_t>;
+  constexpr int bits = ((8 * static_cast<int>(sizeof(Key)) - (sizeof(Key) == 8 ? 1 : 0)) / D) * D;
   unsigned long long* box = nullptr;
-  std::uint32_t *keys = nullptr, *keys2 = nullptr, *idx = nullptr;
+  Key *keys = nullptr, *keys2 = nullptr;
+  std::uint32_t* idx = nullptr;
   GK_CUDA(cudaMallocAsync(&box, 2 * D * sizeof(unsigned long long), st));
-  GK_CUDA(cudaMallocAsync(&keys, nq * 4, st));
-  GK_CUDA(cudaMallocAsync(&keys2, nq * 4, st));
+  GK_CUDA(cudaMallocAsync(&keys, nq * sizeof(Key), st));
+  GK_CUDA(cudaMallocAsync(&keys2, nq * sizeof(Key), st));
   GK_CUDA(cudaMallocAsync(&idx, nq * 4, st));
   k_qbox_init<<<1, 32, 0, st>>>(box, D);
   const unsigned gb = static_cast<unsigned>(std::min<std::uint64_t>((nq + 255) / 256, 148 * 8));
   k_qbox<D><<<gb, 256, 0, st>>>(Q, nq, box);
-  int bits = (32 / D) * D;
-  if (D >= 5 && t0) {
-    k_kdkey<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, *t0, keys, idx);
-    bits = 32;
-  } else {
-    k_morton<D><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, box, keys, idx);
-  }
+  k_curve_key<D, Key><<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(Q, nq, box, keys, idx);
   GK_CHECK_LAUNCH();
   void* tmp = nullptr;
   std::size_t tb = 0;
@@ -601,7 +576,7 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
   switch (d) {
 #define GK_D(DD)                                                   \
   case DD:                                                         \
-    order_queries<DD>(q_dev, nq, perm, st, trees.count > 0 ? &trees.t[0] : nullptr);                        \
+    order_queries<DD>(q_dev, nq, perm, st);                        \
     if (ev_k0) GK_CUDA(cudaEventRecord(ev_k0, st));                \
     launch_d<DD>(k, trees, q_dev, perm, nq, ids_dev, d2_dev, ctr, st); \
     if (ev_k1) GK_CUDA(cudaEventRecord(ev_k1, st));                \
