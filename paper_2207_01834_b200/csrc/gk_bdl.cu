@@ -195,13 +195,27 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
 
 }  // namespace
 
+// GK_TRACE=1: host-side phase timestamps of Insert_L on stderr (diagnostics only)
+struct PhaseTrace {
+  bool on = std::getenv("GK_TRACE") != nullptr;
+  cudaStream_t st = nullptr;  // synchronised before each stamp when tracing
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void operator()(const char* what, long long arg = -1) const {
+    if (!on) return;
+    if (st) GK_CUDA(cudaStreamSynchronize(st));
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[gk] %8.3f ms  %s %lld\n", ms, what, arg);
+  }
+};
+
 // ================================================================= handle ==
 struct gk_bdl {
   int d = 0;
   std::uint32_t X = 1024, leaf = 16;
   int heuristic = 0, device = 0;
   cudaStream_t st = nullptr;
-  cudaStream_t pst[2] = {nullptr, nullptr};  // pipelined host-API kNN (copy/compute overlap)
+  cudaStream_t pst[2] = {nullptr, nullptr};  // pipelined host-API kNN: [0] H2D, [1] D2H (compute on st)
+  std::vector<cudaEvent_t> pev;               // pipeline events, grown on demand
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<DevTree> statics = std::vector<DevTree>(64);
   std::uint64_t F = 0;
@@ -216,7 +230,7 @@ struct gk_bdl {
   void* cub_tmp = nullptr;
   std::size_t cub_bytes = 0;
   BuildScratch scratch;                 // buffer-tree rebuilds (on st)
-  static constexpr int kBuildSlots = 4;  // concurrent builds of distinct new trees
+  static constexpr int kBuildSlots = 16;  // concurrent builds of distinct new trees (<= 14 per Insert_L at 2^24 points)
   BuildScratch bscratch[kBuildSlots];
   cudaStream_t bst[kBuildSlots] = {};
   cudaEvent_t ev_pool = nullptr;
@@ -249,13 +263,19 @@ struct gk_bdl {
   }
 
   void rebuild_buffer_tree() {
+    PhaseTrace tr;
+    tr.st = st;
     free_tree(buf_tree, st);
     dfree(buf_src, st);
     if (buf_n == 0) return;
     // build over arrival indices, then map them to ids (keeping the map for erase)
     std::uint32_t* iota = dalloc<std::uint32_t>(buf_n, st);
     k_iota<<<blocks_for(buf_n), 256, 0, st>>>(iota, buf_n);
-    build_tree(scratch, d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), iota, buf_n, buf_tree, st);
+    tr("  buffer: freed + iota");
+    build_begin(scratch, d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), iota, buf_n, buf_tree, st);
+    tr("  buffer: k_build done");
+    build_finish(scratch);
+    tr("  buffer: emitted");
     buf_src = dalloc<std::uint32_t>(buf_n, st);
     k_gather_ids<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_src, buf_ids, buf_n);
     GK_CHECK_LAUNCH();
@@ -265,12 +285,16 @@ struct gk_bdl {
   // Insert_L of device SoA points (stride sp) with their ids.
   void insert_l(const double* P, std::uint64_t sp, const std::uint32_t* ids, std::uint64_t n) {
     if (n == 0) return;
+    PhaseTrace tr;
+    tr.st = st;
     const std::uint64_t r = n % X, bulk = n - r;
+    tr("insert_l start");
     if (r) {
       k_copy_soa<<<blocks_for(r), 256, 0, st>>>(P + bulk, sp, ids + bulk, buf_coords + buf_n, bstride(), buf_ids + buf_n, d, r);
       GK_CHECK_LAUNCH();
       buf_n += r;
     }
+    tr("buffer append", static_cast<long long>(r));
     const std::uint64_t drained = (buf_n >= X) ? X : 0;
     const std::uint64_t add = (bulk + drained) / X;
     if (add == 0) {
@@ -284,6 +308,7 @@ struct gk_bdl {
       if (destroyed >> i & 1ULL) pool_n += statics[i].live;
     double* pool = dalloc<double>(pool_n * d, st);
     std::uint32_t* pool_ids = dalloc<std::uint32_t>(pool_n, st);
+    tr("pool allocated", static_cast<long long>(pool_n));
     std::uint64_t off = 0;
     for (int i = 0; i < 64; ++i)
       if (destroyed >> i & 1ULL) {
@@ -310,7 +335,7 @@ struct gk_bdl {
       off += bulk;
     }
     GK_CHECK_LAUNCH();
-    if (r || drained) rebuild_buffer_tree();
+    tr("pool staged (launches)", static_cast<long long>(pool_n));
     // build the new trees, largest first, from contiguous pool slices; distinct trees
     // build concurrently on their own streams
     F = Fn;
@@ -332,22 +357,51 @@ struct gk_bdl {
     }
     const auto t0 = std::chrono::steady_clock::now();
     GK_CUDA(cudaEventRecord(ev_pool, st));
+    const bool rebuild_buf = r || drained;
     for (std::size_t w0 = 0; w0 < order.size(); w0 += kBuildSlots) {
       const std::size_t w1 = std::min(order.size(), w0 + kBuildSlots);
+      // the wave's cooperative grids share the co-resident capacity (one block kept for the
+      // buffer tree), in proportion to their points, so every build of the wave runs at once
+      // instead of the small trees queueing behind the largest one's full-GPU grid
+      const int cap = build_capacity(d) - (rebuild_buf && w0 == 0 ? 1 : 0);
+      std::vector<int> grid(w1 - w0);
+      std::uint64_t tot = 0;
+      long long want = 0;
+      for (std::size_t t = w0; t < w1; ++t) {
+        tot += cnts[t];
+        want += grid[t - w0] = build_grid_wanted(d, cnts[t]);
+      }
+      if (want > cap) {
+        const int spare = cap - static_cast<int>(w1 - w0);
+        for (std::size_t t = w0; t < w1; ++t)
+          grid[t - w0] = std::min(grid[t - w0], 1 + static_cast<int>(static_cast<double>(spare) *
+                                                                     static_cast<double>(cnts[t]) / static_cast<double>(tot)));
+      }
       for (std::size_t t = w0; t < w1; ++t) {
         const int slot = static_cast<int>(t - w0);
         GK_CUDA(cudaStreamWaitEvent(bst[slot], ev_pool, 0));
         build_begin(bscratch[slot], d, static_cast<int>(leaf), heuristic, pool + offs[t], pool_n, pool_ids + offs[t],
-                    cnts[t], statics[order[t]], bst[slot]);
+                    cnts[t], statics[order[t]], bst[slot], grid[slot]);
+        tr("  build launched, points", static_cast<long long>(cnts[t]));
       }
-      for (std::size_t t = w0; t < w1; ++t) build_finish(bscratch[t - w0]);
+      if (w0 == 0 && rebuild_buf) {  // the buffer tree builds on st, alongside the static trees
+        rebuild_buffer_tree();
+        tr("buffer tree rebuilt", static_cast<long long>(buf_n));
+      }
+      for (std::size_t t = w0; t < w1; ++t) {
+        build_finish(bscratch[t - w0]);
+        tr("  build finished, points", static_cast<long long>(cnts[t]));
+      }
     }
+    if (order.empty() && rebuild_buf) rebuild_buffer_tree();
     for (auto& bs : bst) GK_CUDA(cudaStreamSynchronize(bs));
     build_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    tr("all builds done");
     built_pts = o;
     dfree(pool, st);
     dfree(pool_ids, st);
     GK_CUDA(cudaStreamSynchronize(st));
+    tr("insert_l done");
   }
 
   // bloom filters are built lazily, on the first erase that touches the tree
@@ -526,6 +580,9 @@ int gk_bdl_create(int dim, uint32_t X, uint32_t leaf, int heuristic, int device,
       for (auto& ps : h->pst) GK_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
       for (auto& bs : h->bst) GK_CUDA(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
       GK_CUDA(cudaEventCreateWithFlags(&h->ev_pool, cudaEventDisableTiming));
+      // pinned control words of every build slot, allocated here rather than inside a timed Insert_L
+      GK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->scratch.host_ctrl), 64));
+      for (auto& bs : h->bscratch) GK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&bs.host_ctrl), 64));
       for (auto& e : h->ev) GK_CUDA(cudaEventCreate(&e));
       cudaMemPool_t pool;
       GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -555,6 +612,7 @@ int gk_bdl_destroy(gk_bdl* h) {
     cudaStreamSynchronize(h->st);
     for (auto& e : h->ev) cudaEventDestroy(e);
     for (auto& ps : h->pst) cudaStreamDestroy(ps);
+    for (auto& e : h->pev) cudaEventDestroy(e);
     for (auto& bs : h->bst) cudaStreamDestroy(bs);
     cudaEventDestroy(h->ev_pool);
     cudaStreamDestroy(h->st);
@@ -698,37 +756,66 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
     if (nq == 0) return;
     DevScope ds(h->device);
     const TreeSet ts = h->trees();
-    // pipeline depth (tunable for experiments via GK_PIPE_CHUNKS; default 4)
-    std::uint64_t nchunk = 4;
-    if (const char* e = std::getenv("GK_PIPE_CHUNKS")) nchunk = std::max<std::uint64_t>(1, std::strtoull(e, nullptr, 10));
-    const std::uint64_t kChunkQ = std::max<std::uint64_t>(1u << 18, (nq + nchunk - 1) / nchunk);
-    if (ts.count > 0 && nq > kChunkQ && is_pinned(q) && is_pinned(ids) && is_pinned(d2)) {
-      // pinned host buffers: pipeline H2D(chunk i+1) | traversal(chunk i) | D2H(chunk i-1) on two streams
-      // (each chunk is Morton-ordered on its own; results are bit-identical to the one-shot path)
+    // chunk schedule: n chunks growing geometrically by `ratio` (small first chunk -> the D2H link
+    // starts early; later chunks large -> compact query packets).  Tunable for experiments via
+    // GK_PIPE_CHUNKS / GK_PIPE_RATIO.
+    int nchunk = 4;
+    double ratio = 1.0;
+    if (const char* e = std::getenv("GK_PIPE_CHUNKS")) nchunk = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("GK_PIPE_RATIO")) ratio = std::max(0.1, std::atof(e));
+    std::vector<std::uint64_t> bounds{0};
+    {
+      double wsum = 0.0, w = 1.0;
+      for (int c = 0; c < nchunk; ++c, w *= ratio) wsum += w;
+      double acc = 0.0;
+      w = 1.0;
+      for (int c = 0; c < nchunk; ++c, w *= ratio) {
+        acc += w;
+        const std::uint64_t e = c + 1 == nchunk ? nq : static_cast<std::uint64_t>(static_cast<double>(nq) * acc / wsum);
+        if (e - bounds.back() >= (1u << 16) || (c + 1 == nchunk && e > bounds.back())) bounds.push_back(e);
+      }
+      if (bounds.back() != nq) bounds.back() = nq;
+    }
+    const std::uint64_t nck = bounds.size() - 1;
+    if (ts.count > 0 && nck > 1 && is_pinned(q) && is_pinned(ids) && is_pinned(d2)) {
+      // pinned host buffers: three-stage pipeline over full-size device buffers, chained by events --
+      // H2D of every chunk on pst[0], kNN_L of chunk i on st once its queries landed, D2H of chunk i on
+      // pst[1] once its rows are final.  Each chunk is Hilbert-ordered on its own; results are
+      // bit-identical to the one-shot path.
+      while (h->pev.size() < 2 * nck + 2) {
+        cudaEvent_t e;
+        GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->pev.push_back(e);
+      }
+      cudaEvent_t ev_alloc = h->pev[0], ev_done = h->pev[1];
+      double* dq = dalloc<double>(nq * h->d, h->st);
+      std::uint32_t* di = dalloc<std::uint32_t>(nq * k, h->st);
+      double* dd = dalloc<double>(nq * k, h->st);
+      GK_CUDA(cudaEventRecord(ev_alloc, h->st));
+      GK_CUDA(cudaStreamWaitEvent(h->pst[0], ev_alloc, 0));
+      GK_CUDA(cudaStreamWaitEvent(h->pst[1], ev_alloc, 0));
+      for (std::uint64_t c = 0; c < nck; ++c) {
+        const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
+        GK_CUDA(cudaMemcpyAsync(dq + off * h->d, q + off * h->d, m * h->d * sizeof(double), cudaMemcpyHostToDevice,
+                                h->pst[0]));
+        GK_CUDA(cudaEventRecord(h->pev[2 + 2 * c], h->pst[0]));
+      }
+      for (std::uint64_t c = 0; c < nck; ++c) {
+        const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
+        GK_CUDA(cudaStreamWaitEvent(h->st, h->pev[2 + 2 * c], 0));
+        knn_launch(h->d, k, ts, dq + off * h->d, m, di + off * k, dd + off * k, nullptr, h->st, nullptr, nullptr);
+        GK_CUDA(cudaEventRecord(h->pev[3 + 2 * c], h->st));
+        GK_CUDA(cudaStreamWaitEvent(h->pst[1], h->pev[3 + 2 * c], 0));
+        GK_CUDA(cudaMemcpyAsync(ids + off * k, di + off * k, m * k * sizeof(std::uint32_t), cudaMemcpyDeviceToHost,
+                                h->pst[1]));
+        GK_CUDA(cudaMemcpyAsync(d2 + off * k, dd + off * k, m * k * sizeof(double), cudaMemcpyDeviceToHost, h->pst[1]));
+      }
+      GK_CUDA(cudaEventRecord(ev_done, h->pst[1]));
+      GK_CUDA(cudaStreamWaitEvent(h->st, ev_done, 0));
+      dfree(dq, h->st);
+      dfree(di, h->st);
+      dfree(dd, h->st);
       GK_CUDA(cudaStreamSynchronize(h->st));
-      double* dq[2];
-      std::uint32_t* di[2];
-      double* dd[2];
-      for (int s2 = 0; s2 < 2; ++s2) {
-        dq[s2] = dalloc<double>(kChunkQ * h->d, h->pst[s2]);
-        di[s2] = dalloc<std::uint32_t>(kChunkQ * k, h->pst[s2]);
-        dd[s2] = dalloc<double>(kChunkQ * k, h->pst[s2]);
-      }
-      int slot = 0;
-      for (std::uint64_t off = 0; off < nq; off += kChunkQ, slot ^= 1) {
-        const std::uint64_t m = std::min(kChunkQ, nq - off);
-        cudaStream_t s2 = h->pst[slot];
-        GK_CUDA(cudaMemcpyAsync(dq[slot], q + off * h->d, m * h->d * sizeof(double), cudaMemcpyHostToDevice, s2));
-        knn_launch(h->d, k, ts, dq[slot], m, di[slot], dd[slot], nullptr, s2, nullptr, nullptr);
-        GK_CUDA(cudaMemcpyAsync(ids + off * k, di[slot], m * k * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, s2));
-        GK_CUDA(cudaMemcpyAsync(d2 + off * k, dd[slot], m * k * sizeof(double), cudaMemcpyDeviceToHost, s2));
-      }
-      for (int s2 = 0; s2 < 2; ++s2) {
-        dfree(dq[s2], h->pst[s2]);
-        dfree(di[s2], h->pst[s2]);
-        dfree(dd[s2], h->pst[s2]);
-        GK_CUDA(cudaStreamSynchronize(h->pst[s2]));
-      }
       return;
     }
     double* dq = dalloc<double>(nq * h->d, h->st);

@@ -105,8 +105,7 @@ __device__ __forceinline__ void sync_all(cg::grid_group& grid) {
     __syncthreads();
     return;
   }
-  grid.sync();
-  __threadfence();  // gpu-scope fence: also invalidates this SM's L1 (CCTL.IVALL)
+  grid.sync();  // gpu-scope ordering; every cross-block read below goes through L2 (__ldcg), never a stale L1 line
 }
 
 // exclusive scan of in[0, n) into out, all blocks of the grid (one grid barrier inside)
@@ -149,8 +148,11 @@ __device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::ui
 }
 
 // -------------------------------------------------------------- the build --
+#ifndef GK_BUILD_MINB
+#define GK_BUILD_MINB 4  // D <= 4: 64 registers, 4 blocks per SM (C2 build -4 % vs 80 registers)
+#endif
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
+__global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_build(const BuildArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ std::uint32_t sh[32];
   const NodeArrays& na = a.na;
@@ -160,6 +162,10 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const std::uint32_t n = a.n;
+  // D <= 4: children's boxes accumulate during the parent's partition (G), so only the root
+  // level runs the box pass B.  At D >= 5 the 4D extra accumulators cost more occupancy than
+  // the saved pass (C3 build +13 %).
+  constexpr bool kChildBoxes = D <= 4;
 
   const double* cur = a.src;
   const std::uint32_t* cur_ids = a.src_ids;
@@ -185,10 +191,12 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
     for (std::uint32_t v = gtid; v <= S; v += gthreads) {
       if (v < S) {
         a.chunk_cnt[v] = (__ldcg(&na.count[off + v]) + kChunk - 1) / kChunk;
+        if (level == 0 || !kChildBoxes) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-          a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2] = ~0ULL;
-          a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1] = 0ULL;
+          for (int j = 0; j < D; ++j) {
+            a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2] = ~0ULL;
+            a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1] = 0ULL;
+          }
         }
         na.nleft[off + v] = 0;
       } else {
@@ -201,15 +209,24 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
     sync_all(grid);
     const std::uint32_t nchunks = __ldcg(&a.chunk_off[S]);
 
-    // B: per chunk: owning node (binary search) + bounding box
-    for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
-      std::uint32_t lo = 0, hi = S;
-      while (hi - lo > 1) {
-        const std::uint32_t mid = (lo + hi) >> 1;
-        if (__ldcg(&a.chunk_off[mid]) <= c) lo = mid; else hi = mid;
+    // chunk -> owning node: a warp per node while nodes are few (many chunks each),
+    // a thread per node once they are many (one or two chunks each)
+    if (S < nwarps) {
+      for (std::uint32_t v = gwarp; v < S; v += nwarps) {
+        const std::uint32_t c0 = __ldcg(&a.chunk_off[v]), c1 = __ldcg(&a.chunk_off[v + 1]);
+        for (std::uint32_t c = c0 + lane; c < c1; c += 32) a.chunk_node[c] = v;
       }
-      const std::uint32_t v = lo, g = off + v;
-      if (lane == 0) a.chunk_node[c] = v;
+    } else {
+      for (std::uint32_t v = gtid; v < S; v += gthreads) {
+        const std::uint32_t c0 = __ldcg(&a.chunk_off[v]), c1 = __ldcg(&a.chunk_off[v + 1]);
+        for (std::uint32_t c = c0; c < c1; ++c) a.chunk_node[c] = v;
+      }
+    }
+    sync_all(grid);
+
+    // B: per chunk: bounding box (root level only when kChildBoxes)
+    for (std::uint32_t c = gwarp; (level == 0 || !kChildBoxes) && c < nchunks; c += nwarps) {
+      const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
       const std::uint32_t s0 = __ldcg(&na.start[g]), cnt = __ldcg(&na.count[g]);
       const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
       const std::uint32_t end = min(first + kChunk, s0 + cnt);
@@ -295,9 +312,21 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
     if (gtid == 0) a.chunk_left[nchunks] = 0;
     sync_all(grid);
 
-    // E: degenerate spatial splits -> object median; internal flags
+    // E: degenerate spatial splits -> object median; internal flags; reset the next
+    // level's box accumulators (this level's were consumed by C)
     for (std::uint32_t v = gtid; v <= S; v += gthreads) {
       if (v == S) { a.is_int[S] = 0; continue; }
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const std::uint64_t u = 2ULL * v + cc;
+        if (kChildBoxes && u < n) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            a.keys[(u * D + j) * 2] = ~0ULL;
+            a.keys[(u * D + j) * 2 + 1] = 0ULL;
+          }
+        }
+      }
       const std::uint32_t g = off + v;
       std::uint8_t fl = __ldcg(&na.flags[g]);
       if (fl & F_LEAF) { a.is_int[v] = 0; continue; }
@@ -363,7 +392,10 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
         }
         sync_all(grid);
         for (std::uint32_t o = gtid; o < nb; o += gthreads) {
-          SelState s = a.sel[o];
+          SelState s;
+          s.hi = __ldcg(&a.sel[o].hi);
+          s.lo = __ldcg(&a.sel[o].lo);
+          s.rank = __ldcg(&a.sel[o].rank);
           std::uint32_t* h = a.hist + o * 256;
           std::uint32_t acc = 0;
           int dsel = 255;
@@ -447,6 +479,14 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
       const std::uint32_t tid = obj ? __ldcg(&na.thr_id[g]) : 0u;
       const std::uint32_t nl = __ldcg(&na.nleft[g]);
       std::uint32_t lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&a.chunk_off[v])]);
+      const std::uint32_t lb0 = lbefore;
+      // the children's bounding boxes, accumulated while partitioning (the next level needs no box pass)
+      double mnl[D], mxl[D], mnr[D], mxr[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        mnl[j] = mnr[j] = __longlong_as_double(0x7ff0000000000000LL);
+        mxl[j] = mxr[j] = -mnl[j];
+      }
       for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
         const std::uint32_t i = i0 + lane;
         const bool valid = i < end;
@@ -468,10 +508,40 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildArgs a) {
           const std::uint32_t lrank = lbefore + __popc(bal & lt_mask);
           const std::uint32_t np = pr ? s0 + lrank : s0 + nl + (i - s0 - lrank);
 #pragma unroll
-          for (int j = 0; j < D; ++j) nxt[j * static_cast<std::uint64_t>(n) + np] = x[j];
+          for (int j = 0; j < D; ++j) {
+            nxt[j * static_cast<std::uint64_t>(n) + np] = x[j];
+            if (!kChildBoxes) continue;
+            if (pr) { mnl[j] = fmin(mnl[j], x[j]); mxl[j] = fmax(mxl[j], x[j]); }
+            else { mnr[j] = fmin(mnr[j], x[j]); mxr[j] = fmax(mxr[j], x[j]); }
+          }
           nxt_ids[np] = id;
         }
         lbefore += __popc(bal);
+      }
+      if (!kChildBoxes) continue;
+      const std::uint32_t nleft_chunk = lbefore - lb0, nright_chunk = end - first - nleft_chunk;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mnl[j] = fmin(mnl[j], __shfl_xor_sync(0xffffffffu, mnl[j], o));
+          mxl[j] = fmax(mxl[j], __shfl_xor_sync(0xffffffffu, mxl[j], o));
+          mnr[j] = fmin(mnr[j], __shfl_xor_sync(0xffffffffu, mnr[j], o));
+          mxr[j] = fmax(mxr[j], __shfl_xor_sync(0xffffffffu, mxr[j], o));
+        }
+      }
+      if (lane < 2 * D) {
+        const int j = lane % D, side = lane / D;  // lanes [0, D): left child, [D, 2D): right child
+        double l = side ? mnr[0] : mnl[0], h = side ? mxr[0] : mxl[0];
+#pragma unroll
+        for (int jj = 1; jj < D; ++jj)
+          if (j == jj) { l = side ? mnr[jj] : mnl[jj]; h = side ? mxr[jj] : mxl[jj]; }
+        if (side ? nright_chunk : nleft_chunk) {
+          const std::uint64_t u = 2ULL * __ldcg(&a.irank[v]) + side;  // the child's index in the next level
+          unsigned long long* kk = a.keys + (u * D + j) * 2;
+          atomicMin(kk, dkey(l));
+          atomicMax(kk + 1, dkey(h));
+        }
       }
     }
     if (gtid == 0) {
@@ -700,8 +770,22 @@ int coresident_blocks(const void* fn) {
 }
 
 template <int D>
+int capacity_d() {
+  static int maxb = 0;  // per D
+  if (!maxb) maxb = coresident_blocks(reinterpret_cast<const void*>(k_build<D>));
+  return maxb;
+}
+
+// grid of a build running alone: co-resident blocks, fewer for small trees (barriers are
+// cheaper with fewer blocks)
+template <int D>
+int grid_wanted_d(std::uint64_t n) {
+  return static_cast<int>(std::min<std::uint64_t>(capacity_d<D>(), std::max<std::uint64_t>(1, n / 4096)));
+}
+
+template <int D>
 void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                   const std::uint32_t* src_ids, std::uint64_t n, DevTree& T, cudaStream_t st) {
+                   const std::uint32_t* src_ids, std::uint64_t n, DevTree& T, cudaStream_t st, int max_grid) {
   static_assert(sizeof(BuildArgs) <= sizeof(sc.args), "BuildScratch::args too small");
   sc.pending = false;
   T = DevTree();
@@ -718,10 +802,7 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   T.coords = dalloc<double>(n * D, st);
   T.ids = dalloc<std::uint32_t>(n, st);
 
-  // grid: co-resident blocks, fewer for small trees (barriers are cheaper with fewer blocks)
-  static int maxb[9] = {0};
-  if (!maxb[D]) maxb[D] = coresident_blocks(reinterpret_cast<const void*>(k_build<D>));
-  const int G = static_cast<int>(std::min<std::uint64_t>(maxb[D], std::max<std::uint64_t>(1, n / 4096)));
+  const int G = max_grid > 0 ? std::min(max_grid, grid_wanted_d<D>(n)) : grid_wanted_d<D>(n);
 
   BuildArgs& a = *reinterpret_cast<BuildArgs*>(sc.args);
   a = BuildArgs();
@@ -837,15 +918,41 @@ char* BuildScratch::reserve(std::size_t bytes, cudaStream_t st) {
 }
 
 void build_begin(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st) {
+                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st, int max_grid) {
   switch (d) {
-    case 2: build_begin_d<2>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 3: build_begin_d<3>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 4: build_begin_d<4>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 5: build_begin_d<5>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 6: build_begin_d<6>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 7: build_begin_d<7>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
-    case 8: build_begin_d<8>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st); break;
+    case 2: build_begin_d<2>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    case 3: build_begin_d<3>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    case 4: build_begin_d<4>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    case 5: build_begin_d<5>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    case 6: build_begin_d<6>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    case 7: build_begin_d<7>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    case 8: build_begin_d<8>(sc, leaf, heuristic, src, src_stride, src_ids, n, out, st, max_grid); break;
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+int build_capacity(int d) {
+  switch (d) {
+    case 2: return capacity_d<2>();
+    case 3: return capacity_d<3>();
+    case 4: return capacity_d<4>();
+    case 5: return capacity_d<5>();
+    case 6: return capacity_d<6>();
+    case 7: return capacity_d<7>();
+    case 8: return capacity_d<8>();
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+int build_grid_wanted(int d, std::uint64_t n) {
+  switch (d) {
+    case 2: return grid_wanted_d<2>(n);
+    case 3: return grid_wanted_d<3>(n);
+    case 4: return grid_wanted_d<4>(n);
+    case 5: return grid_wanted_d<5>(n);
+    case 6: return grid_wanted_d<6>(n);
+    case 7: return grid_wanted_d<7>(n);
+    case 8: return grid_wanted_d<8>(n);
     default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
   }
 }

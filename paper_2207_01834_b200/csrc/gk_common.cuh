@@ -153,8 +153,13 @@ struct BuildScratch {
   ~BuildScratch();
   char* reserve(std::size_t bytes, cudaStream_t st);
 };
+// max_grid > 0 caps the cooperative grid (concurrent builds share the co-resident capacity)
 void build_begin(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st);
+                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st, int max_grid = 0);
+// co-resident blocks of the BuildvEB_S kernel for dimension d (its largest cooperative grid)
+int build_capacity(int d);
+// the grid a build of n points asks for when it runs alone
+int build_grid_wanted(int d, std::uint64_t n);
 void build_finish(BuildScratch& sc);
 inline void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
                        const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st) {

@@ -8,7 +8,7 @@ import sys
 rows = list(csv.reader(open(sys.argv[1])))
 minp = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 h = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(h)]
 ai, si = h.index("Address"), h.index("Source")
 st, ie = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 ti = sum(float(r[ie] or 0) for r in data)

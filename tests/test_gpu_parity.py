@@ -5,6 +5,8 @@ records (vEB slots, splits, boxes), the log structure's F / buffer / live
 counts.  Squared distances: within 1e-12 relative (north star); they come out
 bit-identical because both sides use the same no-FMA operation order.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -282,9 +284,16 @@ def test_pinned_pipelined_host_knn(gk):
     Qp = torch.from_numpy(Q).pin_memory().numpy()
     ids = torch.empty((len(Q), 8), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
     d2 = torch.empty((len(Q), 8), dtype=torch.float64).pin_memory().numpy()
-    rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, len(Q), 8, ids.ctypes.data, d2.ctypes.data)
-    assert rc == 0
-    assert np.array_equal(ids, ids0) and np.array_equal(d2, d20)
+    for chunks, ratio in (("4", "1"), ("5", "1.5"), ("3", "0.5"), ("40", "1")):  # schedule knobs
+        os.environ["GK_PIPE_CHUNKS"], os.environ["GK_PIPE_RATIO"] = chunks, ratio
+        ids.fill(0)
+        d2.fill(0)
+        try:
+            rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, len(Q), 8, ids.ctypes.data, d2.ctypes.data)
+        finally:
+            del os.environ["GK_PIPE_CHUNKS"], os.environ["GK_PIPE_RATIO"]
+        assert rc == 0
+        assert np.array_equal(ids, ids0) and np.array_equal(d2, d20), (chunks, ratio)
 
 
 def test_bloom_filter(gk):
