@@ -108,9 +108,10 @@ __device__ __forceinline__ void sync_all(cg::grid_group& grid) {
   grid.sync();  // gpu-scope ordering; every cross-block read below goes through L2 (__ldcg), never a stale L1 line
 }
 
-// exclusive scan of in[0, n) into out, all blocks of the grid (one grid barrier inside)
-__device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::uint32_t* out, std::uint32_t n,
-                          std::uint32_t* bsum, std::uint32_t* sh) {
+// Grid-wide exclusive scans, split in two halves around one grid barrier: every block
+// sums its segment (scan_partial -> bsum[b]), then every block scans its segment from
+// the prefix of the other blocks' sums (scan_finish).  Several arrays share one barrier.
+__device__ void scan_partial(const std::uint32_t* in, std::uint32_t n, std::uint32_t* bsum, std::uint32_t* sh) {
   const std::uint32_t G = gridDim.x, b = blockIdx.x;
   const std::uint32_t seg = (n + G - 1) / G;
   const std::uint32_t lo = min(n, b * seg), hi = min(n, lo + seg);
@@ -118,7 +119,14 @@ __device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::ui
   for (std::uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += __ldcg(&in[i]);
   s = block_sum(s, sh);
   if (threadIdx.x == 0) bsum[b] = s;
-  sync_all(grid);
+}
+
+// map != nullptr: also writes map[c] = i for c in [out[i], out[i] + in[i]) (chunk -> node)
+__device__ void scan_finish(const std::uint32_t* in, std::uint32_t* out, std::uint32_t n, const std::uint32_t* bsum,
+                            std::uint32_t* sh, std::uint32_t* map = nullptr) {
+  const std::uint32_t G = gridDim.x, b = blockIdx.x;
+  const std::uint32_t seg = (n + G - 1) / G;
+  const std::uint32_t lo = min(n, b * seg), hi = min(n, lo + seg);
   std::uint32_t o = 0;
   for (std::uint32_t i = threadIdx.x; i < b; i += blockDim.x) o += __ldcg(&bsum[i]);
   o = block_sum(o, sh);
@@ -142,9 +150,22 @@ __device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::ui
       if (j < w) wpre += t;
       tot += t;
     }
-    if (i < hi) out[i] = carry + wpre + x - v;
+    if (i < hi) {
+      const std::uint32_t e = carry + wpre + x - v;
+      out[i] = e;
+      if (map)
+        for (std::uint32_t c = e; c < e + v; ++c) map[c] = i;
+    }
     carry += tot;
   }
+}
+
+// exclusive scan of in[0, n) into out, all blocks of the grid (one grid barrier inside)
+__device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::uint32_t* out, std::uint32_t n,
+                          std::uint32_t* bsum, std::uint32_t* sh, std::uint32_t* map = nullptr) {
+  scan_partial(in, n, bsum, sh);
+  sync_all(grid);
+  scan_finish(in, out, n, bsum, sh, map);
 }
 
 // -------------------------------------------------------------- the build --
@@ -175,8 +196,17 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
 
   if (gtid == 0) {
     na.start[0] = 0; na.count[0] = n; na.parent[0] = 0xffffffffu;
+    na.nleft[0] = 0;
     a.lvl_off[0] = 0;
     a.ctrl[C_S] = 1;
+    a.ctrl[C_NOBJ] = 0;
+    a.chunk_cnt[0] = (n + kChunk - 1) / kChunk;  // deeper levels' chunk counts are written by F
+    a.chunk_cnt[1] = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      a.keys[j * 2] = ~0ULL;
+      a.keys[j * 2 + 1] = 0ULL;
+    }
   }
   sync_all(grid);
 
@@ -186,120 +216,107 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     if (S == 0 || level >= kMaxLevels) break;
     const std::uint32_t off = __ldcg(&a.lvl_off[level]);
     const int cdim = level % D;
+    const bool box_pass = level == 0 || !kChildBoxes;  // else the parent's G accumulated the boxes
+    const bool spatial_level = a.heuristic != GK_OBJECT_MEDIAN && level < kDepthCap;
 
-    // A: chunk counts, bbox accumulator reset
-    for (std::uint32_t v = gtid; v <= S; v += gthreads) {
-      if (v < S) {
-        a.chunk_cnt[v] = (__ldcg(&na.count[off + v]) + kChunk - 1) / kChunk;
-        if (level == 0 || !kChildBoxes) {
-#pragma unroll
-          for (int j = 0; j < D; ++j) {
-            a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2] = ~0ULL;
-            a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1] = 0ULL;
-          }
-        }
-        na.nleft[off + v] = 0;
-      } else {
-        a.chunk_cnt[S] = 0;
-      }
-    }
-    if (gtid == 0) a.ctrl[C_NOBJ] = 0;
-    sync_all(grid);
-    grid_scan(grid, a.chunk_cnt, a.chunk_off, S + 1, a.bsum, sh);
+    // chunk offsets; with many nodes (one or two chunks each) the scan also writes the
+    // chunk -> node map, with few nodes a warp per node writes it
+    const bool fused_map = S >= nwarps;
+    grid_scan(grid, a.chunk_cnt, a.chunk_off, S + 1, a.bsum, sh, fused_map ? a.chunk_node : nullptr);
     sync_all(grid);
     const std::uint32_t nchunks = __ldcg(&a.chunk_off[S]);
-
-    // chunk -> owning node: a warp per node while nodes are few (many chunks each),
-    // a thread per node once they are many (one or two chunks each)
-    if (S < nwarps) {
+    if (!fused_map) {
       for (std::uint32_t v = gwarp; v < S; v += nwarps) {
         const std::uint32_t c0 = __ldcg(&a.chunk_off[v]), c1 = __ldcg(&a.chunk_off[v + 1]);
         for (std::uint32_t c = c0 + lane; c < c1; c += 32) a.chunk_node[c] = v;
       }
-    } else {
-      for (std::uint32_t v = gtid; v < S; v += gthreads) {
-        const std::uint32_t c0 = __ldcg(&a.chunk_off[v]), c1 = __ldcg(&a.chunk_off[v + 1]);
-        for (std::uint32_t c = c0; c < c1; ++c) a.chunk_node[c] = v;
-      }
     }
-    sync_all(grid);
 
-    // B: per chunk: bounding box (root level only when kChildBoxes)
-    for (std::uint32_t c = gwarp; (level == 0 || !kChildBoxes) && c < nchunks; c += nwarps) {
-      const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
-      const std::uint32_t s0 = __ldcg(&na.start[g]), cnt = __ldcg(&na.count[g]);
-      const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
-      const std::uint32_t end = min(first + kChunk, s0 + cnt);
-      double mn[D], mx[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) { mn[j] = __longlong_as_double(0x7ff0000000000000LL); mx[j] = -mn[j]; }
-      for (std::uint32_t i = first + lane; i < end; i += 32) {
+    // C: node records and split decisions (needs the final boxes)
+    auto node_records = [&]() {
+      for (std::uint32_t v = gtid; v < S; v += gthreads) {
+        const std::uint32_t g = off + v;
+        double lo[D], hi[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          const double x = __ldcg(&cur[j * cur_stride + i]);
-          mn[j] = fmin(mn[j], x);
-          mx[j] = fmax(mx[j], x);
+          lo[j] = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2]));
+          hi[j] = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1]));
+          na.lo[static_cast<std::uint64_t>(g) * D + j] = lo[j];
+          na.hi[static_cast<std::uint64_t>(g) * D + j] = hi[j];
+        }
+        na.level[g] = static_cast<std::uint8_t>(level);
+        if (__ldcg(&na.count[g]) <= static_cast<std::uint32_t>(a.leaf)) {
+          na.flags[g] = F_LEAF;
+          na.split[g] = 0.0;
+        } else if (!spatial_level) {
+          na.flags[g] = F_OBJECT;
+          na.split[g] = 0.0;
+        } else {
+          na.flags[g] = 0;
+          double l = lo[0], h = hi[0];
+#pragma unroll
+          for (int j = 1; j < D; ++j)
+            if (cdim == j) { l = lo[j]; h = hi[j]; }
+          na.split[g] = __dmul_rn(__dadd_rn(l, h), 0.5);  // (lo + hi) / 2 exactly
         }
       }
+    };
+
+    if (box_pass) {
+      if (!fused_map) sync_all(grid);  // B reads the chunk map
+      // B: per chunk: bounding box
+      for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
+        const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+        const std::uint32_t s0 = __ldcg(&na.start[g]), cnt = __ldcg(&na.count[g]);
+        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
+        const std::uint32_t end = min(first + kChunk, s0 + cnt);
+        double mn[D], mx[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
+        for (int j = 0; j < D; ++j) { mn[j] = __longlong_as_double(0x7ff0000000000000LL); mx[j] = -mn[j]; }
+        for (std::uint32_t i = first + lane; i < end; i += 32) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          mn[j] = fmin(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
-          mx[j] = fmax(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
+          for (int j = 0; j < D; ++j) {
+            const double x = __ldcg(&cur[j * cur_stride + i]);
+            mn[j] = fmin(mn[j], x);
+            mx[j] = fmax(mx[j], x);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            mn[j] = fmin(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
+            mx[j] = fmax(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
+          }
+        }
+        if (lane < D) {
+          double l = mn[0], h = mx[0];
+#pragma unroll
+          for (int j = 1; j < D; ++j)
+            if (lane == j) { l = mn[j]; h = mx[j]; }
+          unsigned long long* kk = a.keys + (static_cast<std::uint64_t>(v) * D + lane) * 2;
+          atomicMin(kk, dkey(l));
+          atomicMax(kk + 1, dkey(h));
         }
       }
-      if (lane < D) {
-        double l = mn[0], h = mx[0];
-#pragma unroll
-        for (int j = 1; j < D; ++j)
-          if (lane == j) { l = mn[j]; h = mx[j]; }
-        unsigned long long* kk = a.keys + (static_cast<std::uint64_t>(v) * D + lane) * 2;
-        atomicMin(kk, dkey(l));
-        atomicMax(kk + 1, dkey(h));
-      }
+      sync_all(grid);
+      node_records();
+    } else {
+      node_records();
+      if (!fused_map) sync_all(grid);  // D reads the chunk map
     }
-    sync_all(grid);
 
-    // C: node records and split decisions
-    for (std::uint32_t v = gtid; v < S; v += gthreads) {
-      const std::uint32_t g = off + v;
-      double lo[D], hi[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        lo[j] = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2]));
-        hi[j] = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + j) * 2 + 1]));
-        na.lo[static_cast<std::uint64_t>(g) * D + j] = lo[j];
-        na.hi[static_cast<std::uint64_t>(g) * D + j] = hi[j];
-      }
-      na.level[g] = static_cast<std::uint8_t>(level);
-      if (__ldcg(&na.count[g]) <= static_cast<std::uint32_t>(a.leaf)) {
-        na.flags[g] = F_LEAF;
-        na.split[g] = 0.0;
-      } else if (a.heuristic == GK_OBJECT_MEDIAN || level >= kDepthCap) {
-        na.flags[g] = F_OBJECT;
-        na.split[g] = 0.0;
-      } else {
-        na.flags[g] = 0;
-        double l = lo[0], h = hi[0];
-#pragma unroll
-        for (int j = 1; j < D; ++j)
-          if (cdim == j) { l = lo[j]; h = hi[j]; }
-        na.split[g] = __dmul_rn(__dadd_rn(l, h), 0.5);  // (lo + hi) / 2 exactly
-      }
-    }
-    sync_all(grid);
-
-    // D: spatial left counts per chunk (x_c < s)
+    // D: spatial left counts per chunk (x_c < s); the split is re-derived from the box exactly as C does
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
       const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
-      const std::uint8_t fl = __ldcg(&na.flags[g]);
+      const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
       std::uint32_t cnt = 0;
-      if (!(fl & (F_LEAF | F_OBJECT))) {
-        const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
+      if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf)) {
         const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
         const std::uint32_t end = min(first + kChunk, s0 + nn);
-        const double s = __ldcg(&na.split[g]);
+        const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
+        const double h = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2 + 1]));
+        const double s = __dmul_rn(__dadd_rn(l, h), 0.5);
         const double* xc = cur + cdim * cur_stride;
         for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
           const std::uint32_t i = i0 + lane;
@@ -313,13 +330,13 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     sync_all(grid);
 
     // E: degenerate spatial splits -> object median; internal flags; reset the next
-    // level's box accumulators (this level's were consumed by C)
+    // level's box accumulators (this level's were consumed by C and D)
     for (std::uint32_t v = gtid; v <= S; v += gthreads) {
       if (v == S) { a.is_int[S] = 0; continue; }
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         const std::uint64_t u = 2ULL * v + cc;
-        if (kChildBoxes && u < n) {
+        if (u < n) {
 #pragma unroll
           for (int j = 0; j < D; ++j) {
             a.keys[(u * D + j) * 2] = ~0ULL;
@@ -442,10 +459,12 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       sync_all(grid);
     }
 
-    // scans: BFS child slots (internal ranks) and chunk left-count offsets
-    grid_scan(grid, a.is_int, a.irank, S + 1, a.bsum, sh);
+    // scans (one shared barrier): BFS child slots (internal ranks) and chunk left-count offsets
+    scan_partial(a.is_int, S + 1, a.bsum, sh);
+    scan_partial(a.chunk_left, nchunks + 1, a.bsum + gridDim.x, sh);
     sync_all(grid);
-    grid_scan(grid, a.chunk_left, a.left_scan, nchunks + 1, a.bsum, sh);
+    scan_finish(a.is_int, a.irank, S + 1, a.bsum, sh);
+    scan_finish(a.chunk_left, a.left_scan, nchunks + 1, a.bsum + gridDim.x, sh);
     sync_all(grid);
     const std::uint32_t nint = __ldcg(&a.irank[S]);
     const std::uint32_t next_off = off + S;
@@ -459,6 +478,16 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]), nl = __ldcg(&na.nleft[g]);
       na.start[cb] = s0; na.count[cb] = nl; na.parent[cb] = g;
       na.start[cb + 1] = s0 + nl; na.count[cb + 1] = nn - nl; na.parent[cb + 1] = g;
+      na.nleft[cb] = 0;
+      na.nleft[cb + 1] = 0;
+      // the next level's chunk counts (its first scan input)
+      const std::uint32_t u = cb - next_off;
+      a.chunk_cnt[u] = (nl + kChunk - 1) / kChunk;
+      a.chunk_cnt[u + 1] = (nn - nl + kChunk - 1) / kChunk;
+    }
+    if (gtid == 0) {
+      a.chunk_cnt[2 * nint] = 0;
+      a.ctrl[C_NOBJ] = 0;
     }
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
       const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
@@ -814,7 +843,7 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   a.src_ids = src_ids;
   const std::size_t need = 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) +
                            (cap_level + 1) * 4 * 5 + cap_chunks * 4 * 3 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 +
-                           C_COUNT * 4 + kSelCap * sizeof(SelState) + kSelCap * 256 * 4 + (G + 1) * 4 + 4 * (cap + 1) +
+                           C_COUNT * 4 + kSelCap * sizeof(SelState) + kSelCap * 256 * 4 + (2 * G + 2) * 4 + 4 * (cap + 1) +
                            40 * 256;
   char* base = sc.reserve(need, st);
   std::size_t used = 0;
@@ -856,7 +885,7 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   a.keys = reinterpret_cast<unsigned long long*>(take(cap_level * D * 2 * 8));
   a.sel = reinterpret_cast<SelState*>(take(kSelCap * sizeof(SelState)));
   a.hist = reinterpret_cast<std::uint32_t*>(take(kSelCap * 256 * 4));
-  a.bsum = reinterpret_cast<std::uint32_t*>(take((G + 1) * 4));
+  a.bsum = reinterpret_cast<std::uint32_t*>(take((2 * G + 2) * 4));
   a.int_by_slot = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
   if (used > need) throw Error(GK_ERR_LOGIC, "BuildvEB_S scratch accounting");
 
