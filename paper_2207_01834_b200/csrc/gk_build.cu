@@ -37,6 +37,20 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef GK_BUILD_TIMELINE
+#define GK_BUILD_TIMELINE 0  // 1: per-level device timestamps via printf (diagnostics)
+#endif
+#if GK_BUILD_TIMELINE
+// stamps kept in thread 0's local memory and printed once at the end (printf inside the
+// level loop would delay block 0 and inflate every later phase)
+#define GK_PHASE_STAMP(id)                                                                     \
+  do {                                                                                         \
+    if (gtid == 0 && level < 32) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_st[level][id])); \
+  } while (0)
+#else
+#define GK_PHASE_STAMP(name) do {} while (0)
+#endif
+
 namespace gk {
 namespace {
 
@@ -187,6 +201,13 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   // level runs the box pass B.  At D >= 5 the 4D extra accumulators cost more occupancy than
   // the saved pass (C3 build +13 %).
   constexpr bool kChildBoxes = D <= 4;
+  // partition rounds per loop trip whose loads are in flight together: 2 at D >= 5 (C3 build
+  // -20 %), 1 at D <= 4, where the 64-register budget has no room for a second round
+#ifdef GK_PART_UNROLL
+  constexpr int kPartUnroll = GK_PART_UNROLL;
+#else
+  constexpr int kPartUnroll = D >= 5 ? 2 : 1;
+#endif
 
   const double* cur = a.src;
   const std::uint32_t* cur_ids = a.src_ids;
@@ -211,8 +232,18 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   sync_all(grid);
 
   int level = 0;
+#if GK_BUILD_TIMELINE
+  unsigned long long tl_st[33][5];
+  std::uint32_t tl_S[33];
+#endif
   for (;; ++level) {
     const std::uint32_t S = __ldcg(&a.ctrl[C_S]);
+#if GK_BUILD_TIMELINE
+    if (gtid == 0 && level < 33) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_st[level][0]));
+      tl_S[level] = S;
+    }
+#endif
     if (S == 0 || level >= kMaxLevels) break;
     const std::uint32_t off = __ldcg(&a.lvl_off[level]);
     const int cdim = level % D;
@@ -224,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     const bool fused_map = S >= nwarps;
     grid_scan(grid, a.chunk_cnt, a.chunk_off, S + 1, a.bsum, sh, fused_map ? a.chunk_node : nullptr);
     sync_all(grid);
+    GK_PHASE_STAMP(1);
     const std::uint32_t nchunks = __ldcg(&a.chunk_off[S]);
     if (!fused_map) {
       for (std::uint32_t v = gwarp; v < S; v += nwarps) {
@@ -318,9 +350,16 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
         const double h = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2 + 1]));
         const double s = __dmul_rn(__dadd_rn(l, h), 0.5);
         const double* xc = cur + cdim * cur_stride;
-        for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
-          const std::uint32_t i = i0 + lane;
-          cnt += __popc(__ballot_sync(0xffffffffu, i < end && __ldcg(&xc[i]) < s));
+        constexpr int U = 4;  // loads of U rounds in flight before their ballots (memory-level parallelism)
+        for (std::uint32_t i0 = first; i0 < end; i0 += 32 * U) {
+          double x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const std::uint32_t i = i0 + 32 * u + lane;
+            x[u] = i < end ? __ldcg(&xc[i]) : s;  // s: never counted
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) cnt += __popc(__ballot_sync(0xffffffffu, x[u] < s));
         }
         if (lane == 0 && cnt) atomicAdd(&na.nleft[g], cnt);
       }
@@ -328,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     }
     if (gtid == 0) a.chunk_left[nchunks] = 0;
     sync_all(grid);
+    GK_PHASE_STAMP(2);
 
     // E: degenerate spatial splits -> object median; internal flags; reset the next
     // level's box accumulators (this level's were consumed by C and D)
@@ -361,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       }
     }
     sync_all(grid);
+    GK_PHASE_STAMP(3);
 
     // O: object-median radix select (batches of kSelCap object nodes)
     const std::uint32_t nobj = __ldcg(&a.ctrl[C_NOBJ]);
@@ -466,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     scan_finish(a.is_int, a.irank, S + 1, a.bsum, sh);
     scan_finish(a.chunk_left, a.left_scan, nchunks + 1, a.bsum + gridDim.x, sh);
     sync_all(grid);
+    GK_PHASE_STAMP(4);
     const std::uint32_t nint = __ldcg(&a.irank[S]);
     const std::uint32_t next_off = off + S;
 
@@ -516,36 +558,46 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
         mnl[j] = mnr[j] = __longlong_as_double(0x7ff0000000000000LL);
         mxl[j] = mxr[j] = -mnl[j];
       }
-      for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
-        const std::uint32_t i = i0 + lane;
-        const bool valid = i < end;
-        bool pr = false;
-        double x[D];
-        std::uint32_t id = 0;
-        if (valid) {
+      constexpr int U = kPartUnroll;  // rounds whose loads are in flight together
+      for (std::uint32_t i0 = first; i0 < end; i0 += 32 * U) {
+        double x[U][D];
+        std::uint32_t id[U];
 #pragma unroll
-          for (int j = 0; j < D; ++j) x[j] = __ldcg(&cur[j * cur_stride + i]);
-          id = __ldcg(&cur_ids[i]);
-          double xc = x[0];
+        for (int u = 0; u < U; ++u) {
+          const std::uint32_t i = i0 + 32 * u + lane;
+          if (i < end) {
 #pragma unroll
-          for (int j = 1; j < D; ++j)
-            if (cdim == j) xc = x[j];
-          pr = obj ? (xc < s || (xc == s && id < tid)) : (xc < s);
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, pr);
-        if (valid) {
-          const std::uint32_t lrank = lbefore + __popc(bal & lt_mask);
-          const std::uint32_t np = pr ? s0 + lrank : s0 + nl + (i - s0 - lrank);
-#pragma unroll
-          for (int j = 0; j < D; ++j) {
-            nxt[j * static_cast<std::uint64_t>(n) + np] = x[j];
-            if (!kChildBoxes) continue;
-            if (pr) { mnl[j] = fmin(mnl[j], x[j]); mxl[j] = fmax(mxl[j], x[j]); }
-            else { mnr[j] = fmin(mnr[j], x[j]); mxr[j] = fmax(mxr[j], x[j]); }
+            for (int j = 0; j < D; ++j) x[u][j] = __ldcg(&cur[j * cur_stride + i]);
+            id[u] = __ldcg(&cur_ids[i]);
           }
-          nxt_ids[np] = id;
         }
-        lbefore += __popc(bal);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const std::uint32_t i = i0 + 32 * u + lane;
+          const bool valid = i < end;
+          bool pr = false;
+          if (valid) {
+            double xc = x[u][0];
+#pragma unroll
+            for (int j = 1; j < D; ++j)
+              if (cdim == j) xc = x[u][j];
+            pr = obj ? (xc < s || (xc == s && id[u] < tid)) : (xc < s);
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, pr);
+          if (valid) {
+            const std::uint32_t lrank = lbefore + __popc(bal & lt_mask);
+            const std::uint32_t np = pr ? s0 + lrank : s0 + nl + (i - s0 - lrank);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              nxt[j * static_cast<std::uint64_t>(n) + np] = x[u][j];
+              if (!kChildBoxes) continue;
+              if (pr) { mnl[j] = fmin(mnl[j], x[u][j]); mxl[j] = fmax(mxl[j], x[u][j]); }
+              else { mnr[j] = fmin(mnr[j], x[u][j]); mxr[j] = fmax(mxr[j], x[u][j]); }
+            }
+            nxt_ids[np] = id[u];
+          }
+          lbefore += __popc(bal);
+        }
       }
       if (!kChildBoxes) continue;
       const std::uint32_t nleft_chunk = lbefore - lb0, nright_chunk = end - first - nleft_chunk;
@@ -586,6 +638,17 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     sync_all(grid);
   }
 
+#if GK_BUILD_TIMELINE
+  unsigned long long tv0 = 0;
+  if (gtid == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv0));
+    for (int L = 0; L + 1 <= level && L < 32; ++L)
+      printf("[tl] n=%u grid=%u level %2d S=%7u: scan %6.1f  C+D %6.1f  E %6.1f  scan2 %6.1f  G %6.1f  total %6.1f us\n", n,
+             gridDim.x, L, tl_S[L], (tl_st[L][1] - tl_st[L][0]) * 1e-3, (tl_st[L][2] - tl_st[L][1]) * 1e-3,
+             (tl_st[L][3] - tl_st[L][2]) * 1e-3, (tl_st[L][4] - tl_st[L][3]) * 1e-3, (tl_st[L + 1][0] - tl_st[L][4]) * 1e-3,
+             (tl_st[L + 1][0] - tl_st[L][0]) * 1e-3);
+  }
+#endif
   // ---- vEB slots, top-down.  Depth d is the cut depth of exactly one frame
   // (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
   // pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees
