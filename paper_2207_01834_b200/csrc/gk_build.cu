@@ -58,6 +58,10 @@ constexpr std::uint8_t F_LEAF = 1, F_OBJECT = 2;
 constexpr int kThreads = 256;
 constexpr int kSelCap = 4096;  // object nodes per radix-select batch
 constexpr int kMaxLevels = 256;
+#ifndef GK_CHUNKS_PER_WARP
+#define GK_CHUNKS_PER_WARP 4
+#endif
+constexpr std::uint64_t kChunksPerWarp = GK_CHUNKS_PER_WARP;
 
 __host__ __device__ inline std::uint64_t hyperceiling_u(std::uint64_t x) {
   std::uint64_t p = 1;
@@ -83,6 +87,7 @@ enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_COUNT = 8 };
 struct BuildArgs {
   int leaf, heuristic;
   std::uint32_t n;
+  std::uint32_t kc;  // points per chunk
   const double* src;
   std::uint64_t src_stride;
   const std::uint32_t* src_ids;
@@ -197,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const std::uint32_t n = a.n;
+  const std::uint32_t kc = a.kc;  // points per chunk (the warp work item), sized to the grid
   // D <= 4: children's boxes accumulate during the parent's partition (G), so only the root
   // level runs the box pass B.  At D >= 5 the 4D extra accumulators cost more occupancy than
   // the saved pass (C3 build +13 %).
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     a.lvl_off[0] = 0;
     a.ctrl[C_S] = 1;
     a.ctrl[C_NOBJ] = 0;
-    a.chunk_cnt[0] = (n + kChunk - 1) / kChunk;  // deeper levels' chunk counts are written by F
+    a.chunk_cnt[0] = (n + kc - 1) / kc;  // deeper levels' chunk counts are written by F
     a.chunk_cnt[1] = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
@@ -300,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
         const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
         const std::uint32_t s0 = __ldcg(&na.start[g]), cnt = __ldcg(&na.count[g]);
-        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
-        const std::uint32_t end = min(first + kChunk, s0 + cnt);
+        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+        const std::uint32_t end = min(first + kc, s0 + cnt);
         double mn[D], mx[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) { mn[j] = __longlong_as_double(0x7ff0000000000000LL); mx[j] = -mn[j]; }
@@ -344,8 +350,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
       std::uint32_t cnt = 0;
       if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf)) {
-        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
-        const std::uint32_t end = min(first + kChunk, s0 + nn);
+        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+        const std::uint32_t end = min(first + kc, s0 + nn);
         const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
         const double h = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2 + 1]));
         const double s = __dmul_rn(__dadd_rn(l, h), 0.5);
@@ -424,8 +430,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
           s.hi = __ldcg(&a.sel[o - b0].hi);
           s.lo = __ldcg(&a.sel[o - b0].lo);
           const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
-          const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
-          const std::uint32_t end = min(first + kChunk, s0 + nn);
+          const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+          const std::uint32_t end = min(first + kc, s0 + nn);
           for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
             const std::uint32_t i = i0 + lane;
             int digit = -1;
@@ -481,8 +487,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
         const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
         if ((__ldcg(&na.flags[g]) & (F_LEAF | F_OBJECT)) != F_OBJECT) continue;
         const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
-        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
-        const std::uint32_t end = min(first + kChunk, s0 + nn);
+        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+        const std::uint32_t end = min(first + kc, s0 + nn);
         const double s = __ldcg(&na.split[g]);
         const std::uint32_t tid = __ldcg(&na.thr_id[g]);
         std::uint32_t cnt = 0;
@@ -524,8 +530,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       na.nleft[cb + 1] = 0;
       // the next level's chunk counts (its first scan input)
       const std::uint32_t u = cb - next_off;
-      a.chunk_cnt[u] = (nl + kChunk - 1) / kChunk;
-      a.chunk_cnt[u + 1] = (nn - nl + kChunk - 1) / kChunk;
+      a.chunk_cnt[u] = (nl + kc - 1) / kc;
+      a.chunk_cnt[u + 1] = (nn - nl + kc - 1) / kc;
     }
     if (gtid == 0) {
       a.chunk_cnt[2 * nint] = 0;
@@ -535,8 +541,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
       const std::uint8_t fl = __ldcg(&na.flags[g]);
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
-      const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kChunk;
-      const std::uint32_t end = min(first + kChunk, s0 + nn);
+      const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+      const std::uint32_t end = min(first + kc, s0 + nn);
       if (fl & F_LEAF) {  // finished: positions are final
         for (std::uint32_t i = first + lane; i < end; i += 32) {
 #pragma unroll
@@ -889,18 +895,24 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   if (n >= 0x7fffffffULL) throw Error(GK_ERR_INVALID, "static tree larger than 2^31-2 points");
   const std::uint64_t cap = 2 * n - 1;
   const std::uint64_t cap_level = std::min<std::uint64_t>(cap, n);
-  const std::uint64_t cap_chunks = n / kChunk + cap_level + 2;
 
   T.coords = dalloc<double>(n * D, st);
   T.ids = dalloc<std::uint32_t>(n, st);
 
   const int G = max_grid > 0 ? std::min(max_grid, grid_wanted_d<D>(n)) : grid_wanted_d<D>(n);
+  // chunk size: about kChunksPerWarp chunks per warp at the top levels, so the last round of
+  // chunks is not a mostly idle one (8192 chunks of 1024 points over 3928 warps left 30 % idle)
+  const std::uint64_t warps = static_cast<std::uint64_t>(G) * (kThreads / 32);
+  const std::uint32_t kc = static_cast<std::uint32_t>(
+      std::max<std::uint64_t>(32, ((n + kChunksPerWarp * warps - 1) / (kChunksPerWarp * warps) + 31) & ~std::uint64_t(31)));
 
   BuildArgs& a = *reinterpret_cast<BuildArgs*>(sc.args);
   a = BuildArgs();
   a.leaf = leaf;
   a.heuristic = heuristic;
   a.n = static_cast<std::uint32_t>(n);
+  a.kc = kc;
+  const std::uint64_t cap_chunks = n / kc + cap_level + 2;
   a.src = src;
   a.src_stride = src_stride;
   a.src_ids = src_ids;
