@@ -344,7 +344,32 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       if (!fused_map) sync_all(grid);  // D reads the chunk map
     }
 
+    // Sparse levels (>= 64 chunks per warp, chunks of a few dozen points): the count pass runs
+    // one lane per chunk, 32 chunks of a warp side by side, instead of a warp walking them one
+    // after another (the partition keeps a warp per chunk: lane-private stores do not coalesce)
+    const bool lane_mode = nchunks >= 64u * nwarps;
+
     // D: spatial left counts per chunk (x_c < s); the split is re-derived from the box exactly as C does
+    if (lane_mode) {
+      for (std::uint32_t c = gwarp * 32 + lane; c < ((nchunks + 31) & ~31u); c += nwarps * 32) {
+        if (c >= nchunks) continue;
+        const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+        const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
+        std::uint32_t cnt = 0;
+        if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf)) {
+          const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+          const std::uint32_t end = min(first + kc, s0 + nn);
+          const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
+          const double h = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2 + 1]));
+          const double s = __dmul_rn(__dadd_rn(l, h), 0.5);
+          const double* xc = cur + cdim * cur_stride;
+#pragma unroll 4
+          for (std::uint32_t i = first; i < end; ++i) cnt += __ldcg(&xc[i]) < s ? 1u : 0u;
+          if (cnt) atomicAdd(&na.nleft[g], cnt);
+        }
+        a.chunk_left[c] = cnt;
+      }
+    } else
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
       const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
