@@ -341,7 +341,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 8,
                     "d2h_bytes_per_step": nq * k * (4 + 8)},
-            "gpu_launches": 10 * args.steps,  # k_qbox_init, k_qbox, k_morton, 6 CUB radix-sort kernels, k_knn
+            "gpu_launches": 10 * args.steps,  # k_qbox_init, k_qbox, k_curve_key, 6 CUB radix-sort kernels, k_knn
             "clocks": clk.summary(),
             "build": {"insert_l_points_per_s": len(P) / build_wall, "buildveb_points_per_s": built / (build_ms / 1000.0),
                       "insert_l_ms": 1000 * build_wall, "buildveb_ms": build_ms, "points": built,

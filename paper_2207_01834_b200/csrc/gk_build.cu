@@ -47,8 +47,18 @@ namespace cg = cooperative_groups;
   do {                                                                                         \
     if (gtid == 0 && level < 32) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl_st[level][id])); \
   } while (0)
+#define GK_TL_PRINT(L0)                                                                                      \
+  do {                                                                                                       \
+    if (gtid == 0)                                                                                           \
+      for (int L = (L0); L + 1 <= level && L < 32; ++L)                                                      \
+        printf("[tl] n=%u grid=%u level %2d S=%7u: scan %6.1f  C+D %6.1f  E %6.1f  scan2 %6.1f  G %6.1f  total %6.1f us\n", \
+               n, gridDim.x, L, tl_S[L], (tl_st[L][1] - tl_st[L][0]) * 1e-3, (tl_st[L][2] - tl_st[L][1]) * 1e-3,   \
+               (tl_st[L][3] - tl_st[L][2]) * 1e-3, (tl_st[L][4] - tl_st[L][3]) * 1e-3,                        \
+               (tl_st[L + 1][0] - tl_st[L][4]) * 1e-3, (tl_st[L + 1][0] - tl_st[L][0]) * 1e-3);              \
+  } while (0)
 #else
 #define GK_PHASE_STAMP(name) do {} while (0)
+#define GK_TL_PRINT(L0) do {} while (0)
 #endif
 
 namespace gk {
@@ -62,6 +72,14 @@ constexpr int kMaxLevels = 256;
 #define GK_CHUNKS_PER_WARP 4
 #endif
 constexpr std::uint64_t kChunksPerWarp = GK_CHUNKS_PER_WARP;
+// partition lane groups at sparse levels: 16-lane groups from this many chunks per warp, 8-lane from
+#ifndef GK_GROUP16_CHUNKS
+#define GK_GROUP16_CHUNKS 20
+#endif
+#ifndef GK_GROUP8_CHUNKS
+#define GK_GROUP8_CHUNKS 40
+#endif
+constexpr std::uint32_t kGroup16Chunks = GK_GROUP16_CHUNKS, kGroup8Chunks = GK_GROUP8_CHUNKS;
 
 __host__ __device__ inline std::uint64_t hyperceiling_u(std::uint64_t x) {
   std::uint64_t p = 1;
@@ -82,7 +100,7 @@ struct SelState {
 };
 
 // control words (device)
-enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_COUNT = 8 };
+enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_COUNT = 8 };
 
 struct BuildArgs {
   int leaf, heuristic;
@@ -191,7 +209,11 @@ __device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::ui
 #ifndef GK_BUILD_MINB
 #define GK_BUILD_MINB 4  // D <= 4: 64 registers, 4 blocks per SM (C2 build -4 % vs 80 registers)
 #endif
-template <int D>
+// PH = 0: the dense top levels; the kernel hands over to PH = 1 (same grid, next launch on the
+// stream) at the first sparse level, so that the lane-group partition of the sparse levels does
+// not cost the dense levels registers.  PH = 1 resumes at ctrl[C_LEVEL] (or returns at once when
+// PH = 0 finished the whole build) and runs the remaining levels and the vEB phase.
+template <int D, int PH>
 __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_build(const BuildArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ std::uint32_t sh[32];
@@ -207,6 +229,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   // level runs the box pass B.  At D >= 5 the 4D extra accumulators cost more occupancy than
   // the saved pass (C3 build +13 %).
   constexpr bool kChildBoxes = D <= 4;
+  // lane-group partition at sparse levels (PH = 1) for D <= 4 (C2 build -8 %); at D >= 5 it lost (C3 +4 %)
+  constexpr bool kGroupedSparse = D <= 4;
   // partition rounds per loop trip whose loads are in flight together: 2 at D >= 5 (C3 build
   // -20 %), 1 at D <= 4, where the 64-register budget has no room for a second round
 #ifdef GK_PART_UNROLL
@@ -220,8 +244,21 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   std::uint64_t cur_stride = a.src_stride;
   double* nxt = a.bufA;
   std::uint32_t* nxt_ids = a.idsA;
+  int level = 0;
 
-  if (gtid == 0) {
+  if (PH == 1) {
+    const std::uint32_t l0 = __ldcg(&a.ctrl[C_LEVEL]);
+    if (l0 == 0xffffffffu) return;  // PH = 0 built the whole tree
+    level = static_cast<int>(l0);
+    if (level > 0) {  // ping-pong state at the start of `level` (level 1 reads bufA)
+      const bool odd = (level & 1) != 0;
+      cur = odd ? a.bufA : a.bufB;
+      cur_ids = odd ? a.idsA : a.idsB;
+      cur_stride = n;
+      nxt = odd ? a.bufB : a.bufA;
+      nxt_ids = odd ? a.idsB : a.idsA;
+    }
+  } else if (gtid == 0) {
     na.start[0] = 0; na.count[0] = n; na.parent[0] = 0xffffffffu;
     na.nleft[0] = 0;
     a.lvl_off[0] = 0;
@@ -229,15 +266,15 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     a.ctrl[C_NOBJ] = 0;
     a.chunk_cnt[0] = (n + kc - 1) / kc;  // deeper levels' chunk counts are written by F
     a.chunk_cnt[1] = 0;
+    a.ctrl[C_LEVEL] = 0xffffffffu;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       a.keys[j * 2] = ~0ULL;
       a.keys[j * 2 + 1] = 0ULL;
     }
   }
-  sync_all(grid);
-
-  int level = 0;
+  if (PH == 0) sync_all(grid);
+  [[maybe_unused]] const int level0 = level;
 #if GK_BUILD_TIMELINE
   unsigned long long tl_st[33][5];
   std::uint32_t tl_S[33];
@@ -263,6 +300,13 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     sync_all(grid);
     GK_PHASE_STAMP(1);
     const std::uint32_t nchunks = __ldcg(&a.chunk_off[S]);
+    // Sparse levels (many small chunks per warp): the partition runs in lane groups (PH = 1)
+    const std::uint32_t cpw = nchunks / nwarps;
+    if (PH == 0 && kGroupedSparse && cpw >= kGroup16Chunks) {
+      if (gtid == 0) a.ctrl[C_LEVEL] = static_cast<std::uint32_t>(level);  // PH = 1 redoes this level's scan
+      GK_TL_PRINT(level0);
+      return;
+    }
     if (!fused_map) {
       for (std::uint32_t v = gwarp; v < S; v += nwarps) {
         const std::uint32_t c0 = __ldcg(&a.chunk_off[v]), c1 = __ldcg(&a.chunk_off[v + 1]);
@@ -562,6 +606,111 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       a.chunk_cnt[2 * nint] = 0;
       a.ctrl[C_NOBJ] = 0;
     }
+    // Sparse levels (many small chunks per warp): the warp splits into 32/gl lane groups that
+    // partition as many chunks side by side, so the chunks' dependent metadata loads and their
+    // point loads overlap instead of running one chunk after another
+    const std::uint32_t gl = cpw >= kGroup8Chunks ? 8u : (cpw >= kGroup16Chunks ? 16u : 32u);
+    if (PH == 1 && gl < 32) {
+      const std::uint32_t ngr = 32 / gl, grp = lane / gl, gla = lane % gl;
+      const unsigned gmask = ((1u << gl) - 1u) << (grp * gl);
+      const unsigned below = lt_mask & gmask;
+      const std::uint32_t ncg = (nchunks + ngr - 1) / ngr;
+      for (std::uint32_t cgi = gwarp; cgi < ncg; cgi += nwarps) {
+        const std::uint32_t c = cgi * ngr + grp;
+        std::uint32_t v = 0, g = 0, s0 = 0, first = 0, end = 0;
+        std::uint8_t fl = F_LEAF;
+        if (c < nchunks) {
+          v = __ldcg(&a.chunk_node[c]);
+          g = off + v;
+          fl = __ldcg(&na.flags[g]);
+          s0 = __ldcg(&na.start[g]);
+          const std::uint32_t nn = __ldcg(&na.count[g]);
+          first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+          end = min(first + kc, s0 + nn);
+        }
+        const bool part = !(fl & F_LEAF);
+        if (!part) {  // finished leaf (or no chunk): positions are final
+          for (std::uint32_t i = first + gla; i < end; i += gl) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) a.out[j * static_cast<std::uint64_t>(n) + i] = __ldcg(&cur[j * cur_stride + i]);
+            a.out_ids[i] = __ldcg(&cur_ids[i]);
+          }
+        }
+        const bool obj = (fl & F_OBJECT) != 0;
+        double s = 0.0;
+        std::uint32_t tid = 0, nl = 0, lbefore = 0;
+        if (part) {
+          s = __ldcg(&na.split[g]);
+          tid = obj ? __ldcg(&na.thr_id[g]) : 0u;
+          nl = __ldcg(&na.nleft[g]);
+          lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&a.chunk_off[v])]);
+        }
+        const std::uint32_t lb0 = lbefore;
+        double mnl[D], mxl[D], mnr[D], mxr[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          mnl[j] = mnr[j] = __longlong_as_double(0x7ff0000000000000LL);
+          mxl[j] = mxr[j] = -mnl[j];
+        }
+        const std::uint32_t rounds = part ? (end - first + gl - 1) / gl : 0u;
+        const std::uint32_t maxr = __reduce_max_sync(0xffffffffu, rounds);
+        for (std::uint32_t r = 0; r < maxr; ++r) {
+          const std::uint32_t i = first + r * gl + gla;
+          const bool valid = part && i < end;
+          double x[D];
+          std::uint32_t id = 0;
+          bool pr = false;
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) x[j] = __ldcg(&cur[j * cur_stride + i]);
+            id = __ldcg(&cur_ids[i]);
+            double xc = x[0];
+#pragma unroll
+            for (int j = 1; j < D; ++j)
+              if (cdim == j) xc = x[j];
+            pr = obj ? (xc < s || (xc == s && id < tid)) : (xc < s);
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, pr);
+          if (valid) {
+            const std::uint32_t lrank = lbefore + __popc(bal & below);
+            const std::uint32_t np = pr ? s0 + lrank : s0 + nl + (i - s0 - lrank);
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              nxt[j * static_cast<std::uint64_t>(n) + np] = x[j];
+              if (!kChildBoxes) continue;
+              if (pr) { mnl[j] = fmin(mnl[j], x[j]); mxl[j] = fmax(mxl[j], x[j]); }
+              else { mnr[j] = fmin(mnr[j], x[j]); mxr[j] = fmax(mxr[j], x[j]); }
+            }
+            nxt_ids[np] = id;
+          }
+          lbefore += __popc(bal & gmask);
+        }
+        if (!kChildBoxes) continue;
+        const std::uint32_t nleft_chunk = lbefore - lb0, nright_chunk = end - first - nleft_chunk;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          for (std::uint32_t o = gl >> 1; o > 0; o >>= 1) {  // within the lane group
+            mnl[j] = fmin(mnl[j], __shfl_xor_sync(0xffffffffu, mnl[j], o));
+            mxl[j] = fmax(mxl[j], __shfl_xor_sync(0xffffffffu, mxl[j], o));
+            mnr[j] = fmin(mnr[j], __shfl_xor_sync(0xffffffffu, mnr[j], o));
+            mxr[j] = fmax(mxr[j], __shfl_xor_sync(0xffffffffu, mxr[j], o));
+          }
+        }
+        if (part && gla < 2 * D) {
+          const int j = static_cast<int>(gla) % D, side = static_cast<int>(gla) / D;
+          double l = side ? mnr[0] : mnl[0], h = side ? mxr[0] : mxl[0];
+#pragma unroll
+          for (int jj = 1; jj < D; ++jj)
+            if (j == jj) { l = side ? mnr[jj] : mnl[jj]; h = side ? mxr[jj] : mxl[jj]; }
+          if (side ? nright_chunk : nleft_chunk) {
+            const std::uint64_t u = 2ULL * __ldcg(&a.irank[v]) + side;
+            unsigned long long* kk = a.keys + (u * D + j) * 2;
+            atomicMin(kk, dkey(l));
+            atomicMax(kk + 1, dkey(h));
+          }
+        }
+      }
+    } else
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
       const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
       const std::uint8_t fl = __ldcg(&na.flags[g]);
@@ -669,17 +818,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     sync_all(grid);
   }
 
-#if GK_BUILD_TIMELINE
-  unsigned long long tv0 = 0;
-  if (gtid == 0) {
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv0));
-    for (int L = 0; L + 1 <= level && L < 32; ++L)
-      printf("[tl] n=%u grid=%u level %2d S=%7u: scan %6.1f  C+D %6.1f  E %6.1f  scan2 %6.1f  G %6.1f  total %6.1f us\n", n,
-             gridDim.x, L, tl_S[L], (tl_st[L][1] - tl_st[L][0]) * 1e-3, (tl_st[L][2] - tl_st[L][1]) * 1e-3,
-             (tl_st[L][3] - tl_st[L][2]) * 1e-3, (tl_st[L][4] - tl_st[L][3]) * 1e-3, (tl_st[L + 1][0] - tl_st[L][4]) * 1e-3,
-             (tl_st[L + 1][0] - tl_st[L][0]) * 1e-3);
-  }
-#endif
+  GK_TL_PRINT(level0);
   // ---- vEB slots, top-down.  Depth d is the cut depth of exactly one frame
   // (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
   // pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees
@@ -895,7 +1034,9 @@ int coresident_blocks(const void* fn) {
 template <int D>
 int capacity_d() {
   static int maxb = 0;  // per D
-  if (!maxb) maxb = coresident_blocks(reinterpret_cast<const void*>(k_build<D>));
+  if (!maxb)
+    maxb = std::min(coresident_blocks(reinterpret_cast<const void*>(k_build<D, 0>)),
+                    coresident_blocks(reinterpret_cast<const void*>(k_build<D, 1>)));
   return maxb;
 }
 
@@ -990,7 +1131,8 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   if (used > need) throw Error(GK_ERR_LOGIC, "BuildvEB_S scratch accounting");
 
   void* args[] = {&a};
-  GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D>), dim3(G), dim3(kThreads), args, 0, st));
+  GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D, 0>), dim3(G), dim3(kThreads), args, 0, st));
+  GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D, 1>), dim3(G), dim3(kThreads), args, 0, st));
   GK_CUDA(cudaMemcpyAsync(sc.host_ctrl, a.ctrl, C_COUNT * 4, cudaMemcpyDeviceToHost, st));
   sc.d = D;
   sc.grid = G;
