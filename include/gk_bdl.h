@@ -10,6 +10,9 @@
  *   gk_bdl_erase    <- bdl_erase (Erase_L)                   SPEC.md:581-589, PAPER.md:1255-1269 (Alg. 4)
  *   gk_bdl_knn      <- bdl_knn (kNN_L) over knn_batch/kNN_S
  *                      rows = KnnBuffer::extract() order     geokit/kdtree/knn_buffer.hpp:42-46 (sorted by (d2, id))
+ *   gk_bdl_range    <- kd-tree range search (ball)           PAPER.md:188-190, 204, 230 (
+ *                      SPEC.md:628 leaves it out of geokit's scope)
+ *   gk_bdl_knn_graph <- k-NN graph generator over kNN
  *   point layout    <- Point<D>/PointSet<D>: D doubles, AoS  geokit/core/point.hpp:11-16
  *   ids             <- PointId = uint32, kNoPoint = ~0u       geokit/core/point.hpp:18-19
  *   dim range 2..8  <- dispatch_dim (invalid_argument else)  geokit/core/point.hpp:22-35
@@ -108,6 +111,25 @@ int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32
 /* Instrumented kNN_L (same results) that also counts the work of §8(d). */
 int gk_bdl_knn_counted_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev,
                               gk_knn_counters* counters);
+
+/* Range search (ball; the kd-tree range search of ParGeo): for every
+ * query, every live point p with canonical squared distance d2(q, p) <= r2 (r2 >= 0, +inf allowed).
+ * gk_bdl_range_count: counts[i] = number of rows of query i.
+ * gk_bdl_range: offsets[nq + 1] = exclusive prefix sums of the counts (offsets[nq] = total), rows of
+ * query i at [offsets[i], offsets[i+1]) of ids / d2, sorted by (d2, id).  ids and d2 hold `capacity`
+ * rows; a larger result fails with GK_ERR_INVALID after writing offsets (call again with room).
+ * The _device variant takes device pointers and reports the total in *total. */
+int gk_bdl_range_count(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* counts);
+int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* offsets, uint32_t* ids, double* d2,
+                 uint64_t capacity);
+int gk_bdl_range_device(gk_bdl* h, const double* q_dev, uint64_t nq, double r2, uint64_t* offsets_dev, uint32_t* ids_dev,
+                        double* d2_dev, uint64_t capacity, uint64_t* total);
+
+/* k-NN graph (ParGeo's generator over kd-tree kNN): one row per live point in
+ * ascending id order (row_ids[r] = its id; gk_bdl_info.live rows), holding its k nearest live
+ * points other than itself, sorted by (d2, id), padded with (GK_NO_POINT, +inf).  1 <= k <= 255. */
+int gk_bdl_knn_graph(gk_bdl* h, int k, uint32_t* row_ids, uint32_t* ids, double* d2);
+int gk_bdl_knn_graph_device(gk_bdl* h, int k, uint32_t* row_ids_dev, uint32_t* ids_dev, double* d2_dev);
 
 int gk_bdl_info_get(gk_bdl* h, gk_bdl_info* info);
 /* Export static tree `tree` (0..63) or the buffer tree (-1): canonical nodes in

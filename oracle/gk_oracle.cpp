@@ -599,6 +599,40 @@ static void knn_l(const Bdl& b, const double* Q, std::size_t nq, int k, Id* out_
   }
 }
 
+// Range search (ball) over one tree (the kd-tree range search of PAPER.md:188-190, 204):
+// prune a subtree iff its box's mindist2 > r2; report live leaf points with d2 <= r2.
+static void range_rec(const Tree& T, std::int32_t slot, const double* q, double r2,
+                      std::vector<std::pair<double, Id>>& out) {
+  const Node& nd = T.nodes[slot];
+  if (mindist2(q, nd, T.d) > r2) return;
+  if (nd.kind == 1) {
+    for (std::uint32_t i = nd.start; i < nd.start + nd.count; ++i) {
+      if (T.dead[i]) continue;
+      const double d2 = sqdist(q, &T.pts[static_cast<std::size_t>(i) * T.d], T.d);
+      if (d2 <= r2) out.push_back({d2, T.ids[i]});
+    }
+    return;
+  }
+  range_rec(T, nd.left, q, r2, out);
+  range_rec(T, nd.right, q, r2, out);
+}
+
+// every live tree of the structure (order irrelevant: rows sorted by (d2, id))
+static void range_l(const Bdl& b, const double* Q, std::size_t nq, double r2,
+                    std::vector<std::vector<std::pair<double, Id>>>& res) {
+  std::vector<const Tree*> trees;
+  for (int i = 63; i >= 0; --i)
+    if ((b.F >> i & 1ULL) && b.statics[i].live > 0) trees.push_back(&b.statics[i]);
+  if (b.buf_tree.live > 0) trees.push_back(&b.buf_tree);
+  res.assign(nq, {});
+#pragma omp parallel for schedule(dynamic, 256)
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(nq); ++i) {
+    for (const Tree* T : trees)
+      if (T->root >= 0 && T->live > 0) range_rec(*T, T->root, Q + i * b.d, r2, res[i]);
+    std::sort(res[i].begin(), res[i].end());
+  }
+}
+
 }  // namespace gko
 
 // ===================================================================== C ABI
@@ -794,6 +828,49 @@ std::uint64_t gko_bdl_live(void* h, std::uint32_t* ids, double* pts) {
       if (pts) std::memcpy(pts + i * b->d, src[idx[i].second], sizeof(double) * b->d);
     }
   return idx.size();
+}
+
+// range search: counts (always) and, when ids/d2 are given, the rows (concatenated, sorted by (d2, id))
+std::uint64_t gko_bdl_range(void* h, const double* Q, std::uint64_t nq, double r2, std::uint64_t* counts,
+                            std::uint32_t* ids, double* d2) {
+  std::vector<std::vector<std::pair<double, Id>>> res;
+  range_l(*static_cast<Bdl*>(h), Q, nq, r2, res);
+  std::uint64_t o = 0;
+  for (std::size_t i = 0; i < nq; ++i) {
+    if (counts) counts[i] = res[i].size();
+    for (const auto& e : res[i]) {
+      if (ids) ids[o] = e.second;
+      if (d2) d2[o] = e.first;
+      ++o;
+    }
+  }
+  return o;
+}
+
+// k-NN graph: every live point (ascending id) as a query, kNN_L with k + 1,
+// the point itself dropped (the first entry carrying its id, else the (k+1)-th)
+std::uint64_t gko_bdl_knn_graph(void* h, int k, std::uint32_t* row_ids, std::uint32_t* ids, double* d2) {
+  auto* b = static_cast<Bdl*>(h);
+  const std::uint64_t n = gko_bdl_live(h, nullptr, nullptr);
+  std::vector<Id> rid(n);
+  std::vector<double> pts(n * b->d);
+  gko_bdl_live(h, rid.data(), pts.data());
+  std::vector<Id> ti(n * (k + 1));
+  std::vector<double> td(n * (k + 1));
+  knn_l(*b, pts.data(), n, k + 1, ti.data(), td.data(), nullptr);
+  for (std::uint64_t r = 0; r < n; ++r) {
+    row_ids[r] = rid[r];
+    int o = 0;
+    bool dropped = false;
+    for (int j = 0; j <= k && o < k; ++j) {
+      const Id id = ti[r * (k + 1) + j];
+      if (!dropped && id == rid[r]) { dropped = true; continue; }
+      ids[r * k + o] = id;
+      d2[r * k + o] = td[r * (k + 1) + j];
+      ++o;
+    }
+  }
+  return n;
 }
 
 // ---- brute-force linear-scan oracle: exact (d2, id) top-k

@@ -91,6 +91,10 @@ def lib():
         L.gko_bdl_tree.argtypes = [_P, C.c_int]
         L.gko_bdl_live.restype = _u64
         L.gko_bdl_live.argtypes = [_P, _P, _P]
+        L.gko_bdl_range.restype = _u64
+        L.gko_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P]
+        L.gko_bdl_knn_graph.restype = _u64
+        L.gko_bdl_knn_graph.argtypes = [_P, C.c_int, _P, _P, _P]
         L.gko_brute_knn.argtypes = [C.c_int, _P, _P, _u64, _P, _u64, C.c_int, _P, _P]
         L.gko_set_threads.argtypes = [C.c_int]
         _lib = L
@@ -284,6 +288,23 @@ class BDLTree:
         out = np.zeros(n, np.uint8)
         lib().gko_tree_dead(h, _ptr(out))
         return out.astype(bool)
+
+    def range(self, q: np.ndarray, r2: float):
+        """ball range search: (offsets (n+1,), ids, d2), rows sorted by (d2, id)"""
+        q = np.ascontiguousarray(q, np.float64).reshape(-1, self.d)
+        cnt = np.zeros(len(q), np.uint64)
+        tot = int(lib().gko_bdl_range(self.h, _ptr(q), len(q), float(r2), _ptr(cnt), None, None))
+        ids = np.zeros(max(tot, 1), np.uint32); d2 = np.zeros(max(tot, 1), np.float64)
+        lib().gko_bdl_range(self.h, _ptr(q), len(q), float(r2), _ptr(cnt), _ptr(ids), _ptr(d2))
+        offs = np.zeros(len(q) + 1, np.uint64)
+        offs[1:] = np.cumsum(cnt)
+        return offs, ids[:tot], d2[:tot]
+
+    def knn_graph(self, k: int):
+        n = int(lib().gko_bdl_live(self.h, None, None))
+        rows = np.zeros(n, np.uint32); ids = np.zeros((n, k), np.uint32); d2 = np.zeros((n, k), np.float64)
+        lib().gko_bdl_knn_graph(self.h, k, _ptr(rows), _ptr(ids), _ptr(d2))
+        return rows, ids, d2
 
     def live(self):
         n = int(lib().gko_bdl_live(self.h, None, None))

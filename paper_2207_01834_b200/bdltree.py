@@ -76,6 +76,11 @@ def lib():
         L.gk_bdl_knn.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
         L.gk_bdl_knn_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
         L.gk_bdl_knn_counted_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, C.POINTER(KnnCounters)]
+        L.gk_bdl_range_count.argtypes = [_P, _P, _u64, C.c_double, _P]
+        L.gk_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64]
+        L.gk_bdl_range_device.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64, C.POINTER(_u64)]
+        L.gk_bdl_knn_graph.argtypes = [_P, C.c_int, _P, _P, _P]
+        L.gk_bdl_knn_graph_device.argtypes = [_P, C.c_int, _P, _P, _P]
         L.gk_bdl_info_get.argtypes = [_P, C.POINTER(_Info)]
         L.gk_bdl_tree_export.argtypes = [_P, C.c_int, _P, _P, _P, C.POINTER(_u64), C.POINTER(_u64)]
         L.gk_bdl_bloom_query.argtypes = [_P, C.c_int, _P, _u64, _P]
@@ -129,6 +134,9 @@ class BDLTree:
       insert(P)        Insert_L  (bdl_insert; bdl_build on an empty tree)
       erase(P) -> int  Erase_L   (bdl_erase), returns #points tombstoned
       knn(S, k)        kNN_L     (bdl_knn) -> (ids uint32 (n,k), sqdist float64 (n,k))
+      range(S, r2)     range search (ball) -> (offsets uint64 (n+1,), ids, sqdist) rows sorted by (d2, id)
+      range_count(S, r2) -> counts uint64 (n,)
+      knn_graph(k)     k-NN graph -> (row ids (m,), ids (m,k), sqdist (m,k)), one row per live point
     Device variants take torch CUDA tensors and keep everything in HBM.
     """
 
@@ -178,6 +186,30 @@ class BDLTree:
         _check(lib().gk_bdl_knn(self._h, _ptr(q), q.shape[0], int(k), _ptr(ids), _ptr(d2)))
         return ids, d2
 
+    def range_count(self, queries, r2: float) -> np.ndarray:
+        q = _rows(queries, self.d)
+        out = np.empty(q.shape[0], np.uint64)
+        _check(lib().gk_bdl_range_count(self._h, _ptr(q), q.shape[0], float(r2), _ptr(out)))
+        return out
+
+    def range(self, queries, r2: float):
+        """Ball range search: every live point with d2 <= r2, per query sorted by (d2, id)."""
+        q = _rows(queries, self.d)
+        offs = np.zeros(q.shape[0] + 1, np.uint64)
+        cap = int(self.range_count(q, r2).sum()) if q.shape[0] else 0
+        ids = np.empty(max(cap, 1), np.uint32)
+        d2 = np.empty(max(cap, 1), np.float64)
+        _check(lib().gk_bdl_range(self._h, _ptr(q), q.shape[0], float(r2), _ptr(offs), _ptr(ids), _ptr(d2), cap))
+        return offs, ids[:cap], d2[:cap]
+
+    def knn_graph(self, k: int):
+        n = self.info()["live"]
+        rows = np.empty(n, np.uint32)
+        ids = np.empty((n, k), np.uint32)
+        d2 = np.empty((n, k), np.float64)
+        _check(lib().gk_bdl_knn_graph(self._h, int(k), _ptr(rows), _ptr(ids), _ptr(d2)))
+        return rows, ids, d2
+
     # ------------------------------------------------------------- device API
     def insert_device(self, pts_dev) -> None:
         _check(lib().gk_bdl_insert_device(self._h, _ptr(pts_dev), int(pts_dev.shape[0])))
@@ -196,6 +228,15 @@ class BDLTree:
         _check(lib().gk_bdl_knn_counted_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), int(k), _ptr(ids_dev),
                                                _ptr(d2_dev), C.byref(c)))
         return c.as_dict()
+
+    def range_device(self, q_dev, r2: float, offs_dev, ids_dev, d2_dev, capacity: int) -> int:
+        t = _u64(0)
+        _check(lib().gk_bdl_range_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), float(r2), _ptr(offs_dev),
+                                         _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
+        return int(t.value)
+
+    def knn_graph_device(self, k: int, rows_dev, ids_dev, d2_dev) -> None:
+        _check(lib().gk_bdl_knn_graph_device(self._h, int(k), _ptr(rows_dev), _ptr(ids_dev), _ptr(d2_dev)))
 
     # ------------------------------------------------------------ inspection
     def info(self) -> dict:

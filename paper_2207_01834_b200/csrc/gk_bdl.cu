@@ -29,6 +29,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "gk_common.cuh"
 
 using namespace gk;
@@ -826,6 +828,170 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
     GK_CUDA(cudaMemcpyAsync(ids, di, nq * k * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, h->st));
     GK_CUDA(cudaMemcpyAsync(d2, dd, nq * k * sizeof(double), cudaMemcpyDeviceToHost, h->st));
     dfree(dq, h->st);
+    dfree(di, h->st);
+    dfree(dd, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+// ------------------------------------------------------------ range search --
+// Ball range search over the log structure: counts, then rows.
+static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, double r2,
+                                       unsigned long long* counts_dev, unsigned long long* offs_dev, std::uint32_t* ids_dev,
+                                       double* d2_dev, std::uint64_t capacity) {
+  need(!std::isnan(r2) && r2 >= 0.0, "r2 must be a non-negative squared radius");
+  if (nq >= 0x7fffffffULL) throw Error(GK_ERR_INVALID, "range batch larger than 2^31-1 queries");
+  if (nq == 0) {
+    if (offs_dev) GK_CUDA(cudaMemsetAsync(offs_dev, 0, 8, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    return 0;
+  }
+  const TreeSet ts = h->trees();
+  unsigned long long* cnt = counts_dev ? counts_dev : dalloc<unsigned long long>(nq + 1, h->st);
+  GK_CUDA(cudaMemsetAsync(cnt, 0, (nq + (counts_dev ? 0 : 1)) * 8, h->st));
+  std::uint32_t* perm = nullptr;
+  std::uint64_t total = 0;
+  if (ts.count > 0) {
+    perm = dalloc<std::uint32_t>(nq, h->st);
+    range_order(h->d, q_dev, nq, perm, h->st);
+    range_launch(h->d, ts, q_dev, nq, r2, perm, cnt, nullptr, nullptr, nullptr, false, h->st);
+  }
+  if (offs_dev) {
+    std::size_t tb = 0;
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs_dev, nq + 1, h->st));
+    void* tmp = dalloc<char>(tb, h->st);
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs_dev, nq + 1, h->st));
+    dfree(tmp, h->st);
+    unsigned long long t = 0;
+    GK_CUDA(cudaMemcpyAsync(&t, offs_dev + nq, 8, cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    total = t;
+    if (ids_dev || d2_dev) {
+      if (total > capacity) {
+        if (perm) dfree(perm, h->st);
+        if (!counts_dev) dfree(cnt, h->st);
+        GK_CUDA(cudaStreamSynchronize(h->st));
+        throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
+                                        std::to_string(capacity) + ")");
+      }
+      need(ids_dev && d2_dev, "range rows need both ids and d2");
+      if (total > 0) {
+        range_launch(h->d, ts, q_dev, nq, r2, perm, nullptr, offs_dev, ids_dev, d2_dev, true, h->st);
+        range_sort(ids_dev, d2_dev, total, offs_dev, nq, h->st);
+      }
+    }
+  }
+  if (perm) dfree(perm, h->st);
+  if (!counts_dev) dfree(cnt, h->st);
+  GK_CUDA(cudaStreamSynchronize(h->st));
+  return total;
+}
+
+int gk_bdl_range_count(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* counts) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(nq == 0 || (q && counts), "null buffer");
+    DevScope ds(h->device);
+    if (nq == 0) return;
+    double* dq = dalloc<double>(nq * h->d, h->st);
+    unsigned long long* dc = dalloc<unsigned long long>(nq, h->st);
+    GK_CUDA(cudaMemcpyAsync(dq, q, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    range_device_impl(h, dq, nq, r2, dc, nullptr, nullptr, nullptr, 0);
+    GK_CUDA(cudaMemcpyAsync(counts, dc, nq * 8, cudaMemcpyDeviceToHost, h->st));
+    dfree(dq, h->st);
+    dfree(dc, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* offsets, uint32_t* ids, double* d2,
+                 uint64_t capacity) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(offsets != nullptr && (nq == 0 || q), "null buffer");
+    DevScope ds(h->device);
+    if (nq == 0) {
+      offsets[0] = 0;
+      return;
+    }
+    double* dq = dalloc<double>(nq * h->d, h->st);
+    unsigned long long* doff = dalloc<unsigned long long>(nq + 1, h->st);
+    GK_CUDA(cudaMemcpyAsync(dq, q, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    // count pass first: the rows go to device buffers of exactly the total size
+    const std::uint64_t total = range_device_impl(h, dq, nq, r2, nullptr, doff, nullptr, nullptr, 0);
+    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    if (total > capacity) {
+      dfree(dq, h->st);
+      dfree(doff, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+      throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
+                                      std::to_string(capacity) + ")");
+    }
+    if (total > 0) {
+      need(ids && d2, "null row buffers");
+      std::uint32_t* di = dalloc<std::uint32_t>(total, h->st);
+      double* dd = dalloc<double>(total, h->st);
+      range_device_impl(h, dq, nq, r2, nullptr, doff, di, dd, total);
+      GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
+      GK_CUDA(cudaMemcpyAsync(d2, dd, total * 8, cudaMemcpyDeviceToHost, h->st));
+      dfree(di, h->st);
+      dfree(dd, h->st);
+    }
+    dfree(dq, h->st);
+    dfree(doff, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_range_device(gk_bdl* h, const double* q_dev, uint64_t nq, double r2, uint64_t* offsets_dev, uint32_t* ids_dev,
+                        double* d2_dev, uint64_t capacity, uint64_t* total) {
+  return guard([&] {
+    need(h != nullptr && offsets_dev != nullptr, "null handle/offsets");
+    need(nq == 0 || q_dev, "null queries");
+    DevScope ds(h->device);
+    const std::uint64_t t = range_device_impl(h, q_dev, nq, r2, nullptr, reinterpret_cast<unsigned long long*>(offsets_dev),
+                                              ids_dev, d2_dev, capacity);
+    if (total) *total = t;
+  });
+}
+
+// ---------------------------------------------------------------- kNN graph --
+static void knn_graph_impl(gk_bdl* h, int k, std::uint32_t* row_ids_dev, std::uint32_t* ids_dev, double* d2_dev) {
+  need(k >= 1, "k must be >= 1");
+  if (k + 1 > GK_MAX_K) throw Error(GK_ERR_UNSUPPORTED, "kNN graph needs k + 1 <= " + std::to_string(GK_MAX_K));
+  const std::uint64_t n = h->live_total();
+  if (n == 0) return;
+  const TreeSet ts = h->trees();
+  knn_graph_launch(h->d, k, ts, n, row_ids_dev, ids_dev, d2_dev, h->st);
+  GK_CUDA(cudaStreamSynchronize(h->st));
+}
+
+int gk_bdl_knn_graph_device(gk_bdl* h, int k, uint32_t* row_ids_dev, uint32_t* ids_dev, double* d2_dev) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    DevScope ds(h->device);
+    need(h->live_total() == 0 || (row_ids_dev && ids_dev && d2_dev), "null buffer");
+    knn_graph_impl(h, k, row_ids_dev, ids_dev, d2_dev);
+  });
+}
+
+int gk_bdl_knn_graph(gk_bdl* h, int k, uint32_t* row_ids, uint32_t* ids, double* d2) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    DevScope ds(h->device);
+    const std::uint64_t n = h->live_total();
+    if (n == 0) return;
+    need(row_ids && ids && d2, "null buffer");
+    need(k >= 1, "k must be >= 1");
+    std::uint32_t* dr = dalloc<std::uint32_t>(n, h->st);
+    std::uint32_t* di = dalloc<std::uint32_t>(n * k, h->st);
+    double* dd = dalloc<double>(n * k, h->st);
+    knn_graph_impl(h, k, dr, di, dd);
+    GK_CUDA(cudaMemcpyAsync(row_ids, dr, n * 4, cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaMemcpyAsync(ids, di, n * k * 4, cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaMemcpyAsync(d2, dd, n * k * 8, cudaMemcpyDeviceToHost, h->st));
+    dfree(dr, h->st);
     dfree(di, h->st);
     dfree(dd, h->st);
     GK_CUDA(cudaStreamSynchronize(h->st));

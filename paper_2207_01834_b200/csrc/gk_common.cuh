@@ -176,5 +176,15 @@ void collapse_tree(int d, DevTree& t, cudaStream_t st);
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq,
                 std::uint32_t* ids_dev, double* d2_dev, gk_knn_counters* counters, cudaStream_t st,
                 cudaEvent_t ev_k0, cudaEvent_t ev_k1);
+// range search (ball, d2 <= r2): K2 order, count / fill passes over the same order, per-query sort
+void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st);
+void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const std::uint32_t* perm,
+                  unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, bool fill,
+                  cudaStream_t st);
+void range_sort(std::uint32_t* ids, double* d2, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
+                cudaStream_t st);
+// kNN graph over the n live points of `trees`: rows in ascending id order (row_ids), k neighbours each
+void knn_graph_launch(int d, int k, const TreeSet& trees, std::uint64_t n, std::uint32_t* row_ids, std::uint32_t* ids,
+                      double* d2, cudaStream_t st);
 
 }  // namespace gk

@@ -560,6 +560,191 @@ void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, c
   GK_CUDA(cudaFreeAsync(idx, st));
 }
 
+
+// ------------------------------------------------------------- kNN graph --
+// live points of every tree (coordinate 0 NaN = tombstone), unordered
+__global__ void k_live_gather(const TreeSet ts, int d, double* __restrict__ pts, std::uint32_t* __restrict__ ids,
+                              std::uint32_t* __restrict__ pos, unsigned long long* __restrict__ ctr) {
+  for (int t = 0; t < ts.count; ++t) {
+    const std::uint64_t n = ts.t[t].stride;
+    const double* c = ts.t[t].coords;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+      if (isnan(c[i])) continue;
+      const unsigned long long o = atomicAdd(ctr, 1ULL);
+      for (int j = 0; j < d; ++j) pts[o * d + j] = c[j * n + i];
+      ids[o] = ts.t[t].ids[i];
+      pos[o] = static_cast<std::uint32_t>(o);
+    }
+  }
+}
+// rows in ascending id order: q[r] = pts[src[r]]
+__global__ void k_gather_rows(const double* __restrict__ pts, const std::uint32_t* __restrict__ src, std::uint64_t n, int d,
+                              double* __restrict__ q) {
+  const std::uint64_t r = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  for (int j = 0; j < d; ++j) q[r * d + j] = pts[static_cast<std::uint64_t>(src[r]) * d + j];
+}
+// row r's k neighbours = its k+1 nearest without the point itself (the first entry with the
+// row's id; if k+1 duplicates at distance 0 precede it, the first k entries)
+__global__ void k_drop_self(std::uint64_t n, int k, const std::uint32_t* __restrict__ row_ids,
+                            const std::uint32_t* __restrict__ ti, const double* __restrict__ td,
+                            std::uint32_t* __restrict__ oi, double* __restrict__ od) {
+  const std::uint64_t r = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  const std::uint32_t self = row_ids[r];
+  const std::uint64_t a = r * (k + 1), b = r * k;
+  int o = 0;
+  bool dropped = false;
+  for (int j = 0; j <= k && o < k; ++j) {
+    const std::uint32_t id = ti[a + j];
+    if (!dropped && id == self) { dropped = true; continue; }
+    oi[b + o] = id;
+    od[b + o] = td[a + j];
+    ++o;
+  }
+}
+
+// ------------------------------------------------------- range search (ball) --
+// ParGeo's kd-tree range search (Table 1), over the log
+// structure like kNN_L: every live point p with canonical d2(q, p) <= r2.  The same
+// packet traversal as K1 with a fixed threshold: a child is entered when any lane's
+// fp32 box lower bound is <= r2 rounded up (conservative), a staged leaf point is
+// reported when its exact fp64 d2 <= r2.  FILL = false counts per query, FILL = true
+// writes each query's rows at its offset (traversal order; sorted afterwards).
+template <int D, bool FILL>
+__global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* __restrict__ Q,
+                                               const std::uint32_t* __restrict__ perm, std::uint64_t nq, double r2,
+                                               unsigned long long* __restrict__ counts,
+                                               const unsigned long long* __restrict__ offs,
+                                               std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
+                                               unsigned* __restrict__ tile_ctr) {
+  constexpr int kWarps = 8;
+  __shared__ std::uint64_t s_stack[kWarps][kStack];
+  __shared__ __align__(16) double s_pts[kWarps][D * GK_MAX_LEAF];
+  __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const unsigned ntiles = static_cast<unsigned>((nq + 31) / 32);
+  while (true) {
+    unsigned tile = 0;
+    if (lane == 0) tile = atomicAdd(tile_ctr, 1u);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= ntiles) break;
+    const std::uint64_t qi = static_cast<std::uint64_t>(tile) * 32 + lane;
+    const bool active = qi < nq;
+    std::uint32_t orig = 0;
+    double q[D];
+    unsigned long long qlo2[D], qhi2[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) q[j] = 0.0;
+    if (active) {
+      orig = perm[qi];
+#pragma unroll
+      for (int j = 0; j < D; ++j) q[j] = Q[static_cast<std::uint64_t>(orig) * D + j];
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const float lo = __double2float_rd(q[j]), hi = __double2float_ru(q[j]);
+      qlo2[j] = pk2(lo, lo);
+      qhi2[j] = pk2(hi, hi);
+    }
+    const float rf = active ? __double2float_ru(r2) : -1.f;
+    const double rq = active ? r2 : -1.0;
+    unsigned long long cnt = 0;
+    const unsigned long long base = (FILL && active) ? offs[orig] : 0ULL;
+    for (int t = 0; t < ts.count; ++t) {
+      const float4* __restrict__ nodes = static_cast<const float4*>(ts.t[t].tnodes);
+      const double* __restrict__ coords = ts.t[t].coords;
+      const std::uint32_t* __restrict__ ids = ts.t[t].ids;
+      const std::uint64_t stride = ts.t[t].stride;
+      std::uint64_t ref = ts.t[t].root;
+      int sp = 0;
+      while (true) {
+        if (is_leaf_ref(ref)) {
+          const std::uint32_t c = leaf_count(ref);
+          const std::uint64_t s = leaf_start(ref);
+          __syncwarp();
+          if (lane < static_cast<int>(c)) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) s_pts[w][j * GK_MAX_LEAF + lane] = coords[j * stride + s + lane];
+            if (FILL) s_ids[w][lane] = ids[s + lane];
+          }
+          __syncwarp();
+          for (std::uint32_t p = 0; p < c; ++p) {
+            double tt = __dsub_rn(q[0], s_pts[w][p]);
+            double d2 = __dmul_rn(tt, tt);
+#pragma unroll
+            for (int j = 1; j < D; ++j) {
+              tt = __dsub_rn(q[j], s_pts[w][j * GK_MAX_LEAF + p]);
+              d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
+            }
+            if (d2 <= rq) {  // NaN (tombstone) never qualifies
+              if (FILL) {
+                out_ids[base + cnt] = s_ids[w][p];
+                out_d2[base + cnt] = d2;
+              }
+              ++cnt;
+            }
+          }
+        } else {
+          const float4* nd = nodes + ref * (D + 1);
+          unsigned long long u[2 * (D + 1)];
+#pragma unroll
+          for (int v = 0; v <= D; ++v) {
+            const ulonglong2 x = reinterpret_cast<const ulonglong2*>(nd)[v];
+            u[2 * v] = x.x;
+            u[2 * v + 1] = x.y;
+          }
+          float m0, m1;
+          box_lb_pair<D>(qlo2, qhi2, u, u + D, m0, m1);
+          const unsigned b0 = __ballot_sync(0xffffffffu, m0 <= rf), b1 = __ballot_sync(0xffffffffu, m1 <= rf);
+          if (b0 && b1) {
+            if (lane == 0) s_stack[w][sp] = u[2 * D + 1];
+            ++sp;
+            ref = u[2 * D];
+            continue;
+          } else if (b0) {
+            ref = u[2 * D];
+            continue;
+          } else if (b1) {
+            ref = u[2 * D + 1];
+            continue;
+          }
+        }
+        // the threshold never changes: every pushed subtree is still wanted by some lane
+        __syncwarp();
+        if (sp == 0) break;
+        ref = s_stack[w][--sp];
+      }
+    }
+    if (active && !FILL) counts[orig] = cnt;
+  }
+}
+
+template <int D>
+void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, unsigned long long* counts,
+             unsigned long long* offs, std::uint32_t* ids, double* d2, bool fill, std::uint32_t* perm, cudaStream_t st) {
+  static int grid = 0;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    int dev = 0, sms = 0, per0 = 0, per1 = 0;
+    GK_CUDA(cudaGetDevice(&dev));
+    GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k_range<D, false>, 256, 0));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_range<D, true>, 256, 0));
+    grid = std::max(1, std::min(per0, per1)) * sms;
+  });
+  const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(grid, (nq + 255) / 256));
+  unsigned* tile_ctr = nullptr;
+  GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
+  GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
+  if (fill) k_range<D, true><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr);
+  else k_range<D, false><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr);
+  GK_CHECK_LAUNCH();
+  GK_CUDA(cudaFreeAsync(tile_ctr, st));
+}
+
 }  // namespace
 
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq, std::uint32_t* ids_dev,
@@ -601,6 +786,102 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
     GK_CUDA(cudaFreeAsync(ctr, st));
   }
   GK_CUDA(cudaFreeAsync(perm, st));
+}
+
+void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st) {
+  switch (d) {
+#define GK_D(DD) case DD: order_queries<DD>(q_dev, nq, perm, st); break;
+    GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const std::uint32_t* perm,
+                  unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, bool fill,
+                  cudaStream_t st) {
+  if (nq == 0) return;
+  switch (d) {
+#define GK_D(DD)                                                                                                \
+  case DD:                                                                                                      \
+    range_d<DD>(trees, q_dev, nq, r2, counts, const_cast<unsigned long long*>(offs), ids, d2, fill,            \
+                const_cast<std::uint32_t*>(perm), st);                                                          \
+    break;
+    GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+// Each query's rows sorted by (d2, id): an id sort, then a stable d2 sort, per segment.
+void range_sort(std::uint32_t* ids, double* d2, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
+                cudaStream_t st) {
+  if (total == 0) return;
+  if (total > 0x7fffffffULL || nq > 0x7fffffffULL)
+    throw Error(GK_ERR_UNSUPPORTED, "range result larger than 2^31-1 rows");
+  std::uint32_t* ids2 = nullptr;
+  double* d22 = nullptr;
+  GK_CUDA(cudaMallocAsync(&ids2, total * 4, st));
+  GK_CUDA(cudaMallocAsync(&d22, total * 8, st));
+  const int ni = static_cast<int>(total), ns = static_cast<int>(nq);
+  std::size_t b1 = 0, b2 = 0;
+  GK_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, b1, ids, ids2, d2, d22, ni, ns, offs, offs + 1, st));
+  GK_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, b2, d22, d2, ids2, ids, ni, ns, offs, offs + 1, st));
+  void* tmp = nullptr;
+  GK_CUDA(cudaMallocAsync(&tmp, std::max(b1, b2), st));
+  std::size_t tb = std::max(b1, b2);
+  GK_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp, tb, ids, ids2, d2, d22, ni, ns, offs, offs + 1, st));
+  tb = std::max(b1, b2);
+  GK_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp, tb, d22, d2, ids2, ids, ni, ns, offs, offs + 1, st));
+  GK_CUDA(cudaFreeAsync(tmp, st));
+  GK_CUDA(cudaFreeAsync(ids2, st));
+  GK_CUDA(cudaFreeAsync(d22, st));
+}
+
+// kNN graph (ParGeo's k-NN graph generator over kd-tree kNN): every live point
+// as a query (rows in ascending id order), kNN_L with k + 1, the point itself dropped.
+void knn_graph_launch(int d, int k, const TreeSet& ts, std::uint64_t n, std::uint32_t* row_ids, std::uint32_t* ids,
+                      double* d2, cudaStream_t st) {
+  if (n == 0) return;
+  if (n >= 0xffffffffULL) throw Error(GK_ERR_INVALID, "kNN graph over more than 2^32-1 points");
+  double *pts = nullptr, *q = nullptr, *td = nullptr;
+  std::uint32_t *uid = nullptr, *pos = nullptr, *src = nullptr, *ti = nullptr;
+  unsigned long long* ctr = nullptr;
+  GK_CUDA(cudaMallocAsync(&pts, n * d * 8, st));
+  GK_CUDA(cudaMallocAsync(&q, n * d * 8, st));
+  GK_CUDA(cudaMallocAsync(&uid, n * 4, st));
+  GK_CUDA(cudaMallocAsync(&pos, n * 4, st));
+  GK_CUDA(cudaMallocAsync(&src, n * 4, st));
+  GK_CUDA(cudaMallocAsync(&ctr, 8, st));
+  GK_CUDA(cudaMemsetAsync(ctr, 0, 8, st));
+  k_live_gather<<<static_cast<unsigned>(std::min<std::uint64_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(ts, d, pts, uid,
+                                                                                                          pos, ctr);
+  GK_CHECK_LAUNCH();
+  unsigned long long got = 0;
+  GK_CUDA(cudaMemcpyAsync(&got, ctr, 8, cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  if (got != n) throw Error(GK_ERR_LOGIC, "kNN graph: live point count mismatch");
+  void* tmp = nullptr;
+  std::size_t tb = 0;
+  GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, uid, row_ids, pos, src, static_cast<int>(n), 0, 32, st));
+  GK_CUDA(cudaMallocAsync(&tmp, tb, st));
+  GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, uid, row_ids, pos, src, static_cast<int>(n), 0, 32, st));
+  k_gather_rows<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pts, src, n, d, q);
+  GK_CHECK_LAUNCH();
+  GK_CUDA(cudaFreeAsync(tmp, st));
+  GK_CUDA(cudaFreeAsync(pts, st));
+  GK_CUDA(cudaFreeAsync(uid, st));
+  GK_CUDA(cudaFreeAsync(pos, st));
+  GK_CUDA(cudaFreeAsync(src, st));
+  GK_CUDA(cudaFreeAsync(ctr, st));
+  GK_CUDA(cudaMallocAsync(&ti, n * (k + 1) * 4, st));
+  GK_CUDA(cudaMallocAsync(&td, n * (k + 1) * 8, st));
+  knn_launch(d, k + 1, ts, q, n, ti, td, nullptr, st, nullptr, nullptr);
+  k_drop_self<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, k, row_ids, ti, td, ids, d2);
+  GK_CHECK_LAUNCH();
+  GK_CUDA(cudaFreeAsync(q, st));
+  GK_CUDA(cudaFreeAsync(ti, st));
+  GK_CUDA(cudaFreeAsync(td, st));
 }
 
 }  // namespace gk

@@ -1,0 +1,143 @@
+"""GPU parity for the §8f-4 consumers of the kd-trees: ball range search and the
+k-NN graph, through the C ABI against the oracle.
+
+Rows are bit-exact: ids, the per-query row order (d2, id) and the squared
+distances (same no-FMA canonical arithmetic on both sides; RTOL kept as the
+north-star bound)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-12
+
+
+def _same(a, b, what):
+    for x, y, name in zip(a, b, ("offsets", "ids", "d2")):
+        assert x.shape == y.shape, f"{what}: {name} shape {x.shape} vs {y.shape}"
+        if name == "d2":
+            fin = np.isfinite(y)
+            assert np.array_equal(np.isfinite(x), fin), what
+            rel = np.abs(x[fin] - y[fin]) / np.maximum(np.abs(y[fin]), 1e-300)
+            assert (rel <= RTOL).all(), f"{what}: max rel {rel.max()}"
+        else:
+            bad = np.nonzero(x != y)[0]
+            assert len(bad) == 0, f"{what}: {name} differs at {bad[:5]}"
+
+
+def _pair(gk, oracle, d, X=1024, leaf=16, heur=0):
+    return gk.BDLTree(d, X=X, leaf_size=leaf, heuristic=heur), oracle.BDLTree(d, X=X, leaf=leaf, heuristic=heur)
+
+
+@pytest.mark.parametrize("d", [2, 3, 5, 7, 8])
+def test_range_parity(gk, oracle, d):
+    rng = np.random.default_rng(100 + d)
+    g, o = _pair(gk, oracle, d, X=256, leaf=8)
+    P = rng.random((20_000, d))
+    P[15_000:15_500] = P[:500]  # duplicates
+    for part in np.array_split(P, 3):
+        g.insert(part); o.insert(part)
+    E = P[rng.choice(len(P), 2_000, replace=False)]
+    assert g.erase(E) == o.erase(E)
+    Q = np.concatenate([rng.random((3_000, d)), P[:500]])
+    # r2 giving ~ 0, ~ 1, ~ 20 points per query, then exact duplicates only
+    vol = {2: np.pi, 3: 4.18879, 5: 5.26379, 7: 4.72477, 8: 4.05871}[d]
+    for mean in (0.5, 20.0):
+        r2 = float((mean / len(P) / vol) ** (2.0 / d))
+        _same(g.range(Q, r2), o.range(Q, r2), f"d={d} r2={r2}")
+        assert np.array_equal(g.range_count(Q, r2), np.diff(o.range(Q, r2)[0]))
+    _same(g.range(Q, 0.0), o.range(Q, 0.0), f"d={d} r2=0")
+
+
+def test_range_edges(gk, oracle):
+    g, o = _pair(gk, oracle, 3)
+    Q = np.random.default_rng(1).random((50, 3))
+    offs, ids, d2 = g.range(Q, 1.0)  # empty structure
+    assert not offs.any() and len(ids) == 0
+    P = np.random.default_rng(2).random((3_000, 3))
+    g.insert(P); o.insert(P)
+    _same(g.range(Q, np.inf), o.range(Q, np.inf), "r2=inf")  # every live point, sorted
+    offs, ids, d2 = g.range(Q[:0], 1.0)
+    assert offs.tolist() == [0]
+    with pytest.raises(ValueError):
+        g.range(Q, -1.0)
+    with pytest.raises(ValueError):
+        g.range(Q, float("nan"))
+    # a too-small capacity fails after writing the offsets
+    import ctypes as C
+    lib = gk.lib()
+    offs = np.zeros(len(Q) + 1, np.uint64)
+    ids = np.zeros(4, np.uint32); d2 = np.zeros(4, np.float64)
+    rc = lib.gk_bdl_range(g._h, Q.ctypes.data_as(C.c_void_p), len(Q), 0.05, offs.ctypes.data_as(C.c_void_p),
+                          ids.ctypes.data_as(C.c_void_p), d2.ctypes.data_as(C.c_void_p), 4)
+    assert rc == 1 and int(offs[-1]) == int(o.range(Q, 0.05)[0][-1]) > 4
+
+
+def test_range_device(gk, oracle):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(7)
+    g, o = _pair(gk, oracle, 3)
+    P = rng.random((50_000, 3))
+    g.insert(P); o.insert(P)
+    Q = rng.random((10_000, 3))
+    r2 = 1e-3
+    want = o.range(Q, r2)
+    total = int(want[0][-1])
+    qd = torch.from_numpy(Q).cuda()
+    offs = torch.zeros(len(Q) + 1, dtype=torch.int64, device="cuda")
+    ids = torch.zeros(total, dtype=torch.int32, device="cuda")
+    d2 = torch.zeros(total, dtype=torch.float64, device="cuda")
+    assert g.range_device(qd, r2, offs, ids, d2, total) == total
+    got = (offs.cpu().numpy().view(np.uint64), ids.cpu().numpy().view(np.uint32), d2.cpu().numpy())
+    _same(got, want, "device")
+
+
+@pytest.mark.parametrize("d,k", [(2, 1), (3, 10), (7, 16), (3, 255)])
+def test_knn_graph_parity(gk, oracle, d, k):
+    rng = np.random.default_rng(200 + d + k)
+    g, o = _pair(gk, oracle, d, X=128, leaf=16)
+    n = 2_000 if k == 255 else 12_000
+    P = rng.random((n, d))
+    P[n - 300:] = P[:300]  # duplicates at distance 0 with other ids
+    for part in np.array_split(P, 4):
+        g.insert(part); o.insert(part)
+    E = P[rng.choice(n, n // 10, replace=False)]
+    assert g.erase(E) == o.erase(E)
+    gr, gi, gd = g.knn_graph(k)
+    orr, oi, od = o.knn_graph(k)
+    assert np.array_equal(gr, orr)
+    assert np.array_equal(gi, oi), f"{np.nonzero((gi != oi).any(1))[0][:5]}"
+    assert np.array_equal(np.isfinite(gd), np.isfinite(od))
+    fin = np.isfinite(od)
+    assert (np.abs(gd[fin] - od[fin]) <= RTOL * np.maximum(od[fin], 1e-300)).all()
+    assert not (gi == gr[:, None]).any(), "a row lists its own point"
+
+
+def test_knn_graph_edges(gk, oracle):
+    g, o = _pair(gk, oracle, 3)
+    rows, ids, d2 = g.knn_graph(3)  # empty
+    assert rows.shape == (0,) and ids.shape == (0, 3)
+    g.insert(np.array([[0.5, 0.5, 0.5]])); o.insert(np.array([[0.5, 0.5, 0.5]]))
+    rows, ids, d2 = g.knn_graph(3)  # one point: all padding
+    assert rows.tolist() == [0] and (ids == 0xFFFFFFFF).all() and np.isinf(d2).all()
+    with pytest.raises(NotImplementedError):
+        g.knn_graph(256)
+    with pytest.raises(ValueError):
+        g.knn_graph(0)
+
+
+def test_knn_graph_device(gk, oracle):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(9)
+    g, o = _pair(gk, oracle, 3)
+    P = rng.random((30_000, 3))
+    g.insert(P); o.insert(P)
+    n, k = len(P), 8
+    rows = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ids = torch.zeros((n, k), dtype=torch.int32, device="cuda")
+    d2 = torch.zeros((n, k), dtype=torch.float64, device="cuda")
+    g.knn_graph_device(k, rows, ids, d2)
+    orr, oi, od = o.knn_graph(k)
+    assert np.array_equal(rows.cpu().numpy().view(np.uint32), orr)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), oi)
+    assert np.array_equal(d2.cpu().numpy(), od)

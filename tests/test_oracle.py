@@ -206,3 +206,57 @@ def test_determinism_across_threads(oracle):
         assert np.array_equal(r[0], res[0][0]) and np.array_equal(r[1], res[0][1])
     for r in res[3::2]:
         assert r[0] == res[1][0] and np.array_equal(r[1], res[1][1])
+
+
+# --------------------------------------------------- §8f-4: range search, kNN graph
+def _brute_d2(P, q):
+    """canonical d2 (sum_j (q_j - p_j)^2, left to right, no FMA) of every row of P"""
+    t = q[0] - P[:, 0]
+    s = t * t
+    for j in range(1, P.shape[1]):
+        t = q[j] - P[:, j]
+        s = s + t * t
+    return s
+
+
+def _small_structure(oracle, d, seed):
+    rng = np.random.default_rng(seed)
+    o = oracle.BDLTree(d, X=64, leaf=4)
+    P = rng.random((700, d))
+    P[500:540] = P[:40]  # exact duplicates (distinct ids)
+    o.insert(P[:300])
+    o.insert(P[300:])
+    o.erase(P[rng.choice(700, 90, replace=False)])  # tombstones, collapses, reinsertions
+    return o, rng
+
+
+@pytest.mark.parametrize("d", [2, 3, 7])
+def test_range_oracle_vs_brute(oracle, d):  # PAPER.md:188-190, 204 (kd-tree range search)
+    o, rng = _small_structure(oracle, d, 11 + d)
+    ids_live, P = o.live()
+    Q = np.concatenate([rng.random((60, d)), P[:20]])
+    for r2 in (0.0, 0.01, 0.2, np.inf):
+        offs, ids, d2 = o.range(Q, r2)
+        for i, q in enumerate(Q):
+            dd = _brute_d2(P, q)
+            m = dd <= r2
+            order = np.lexsort((ids_live[m], dd[m]))
+            a, b = int(offs[i]), int(offs[i + 1])
+            assert np.array_equal(ids[a:b], ids_live[m][order]), (r2, i)
+            assert np.array_equal(d2[a:b], dd[m][order]), (r2, i)
+
+
+@pytest.mark.parametrize("k", [1, 5, 17])
+def test_knn_graph_oracle_vs_brute(oracle, k):  # PAPER.md:202-203 (k-NN graph generator)
+    o, _ = _small_structure(oracle, 3, 5 + k)
+    ids_live, P = o.live()
+    rows, ids, d2 = o.knn_graph(k)
+    assert np.array_equal(rows, ids_live)
+    for r in range(len(rows)):
+        dd = _brute_d2(P, P[r])
+        keep = np.arange(len(P)) != r
+        order = np.lexsort((ids_live[keep], dd[keep]))[:k]
+        want_i = ids_live[keep][order]
+        want_d = dd[keep][order]
+        assert np.array_equal(ids[r, :len(want_i)], want_i), r
+        assert np.array_equal(d2[r, :len(want_d)], want_d), r
