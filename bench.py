@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the range-search / kNN-graph lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time for cpu_baseline")
     return ap.parse_args()
 
@@ -301,6 +302,50 @@ def run_gpu(args):
     e2e_t = max_over_ranks(sum(e2e_s), device=dev)
     e2e = whole_job_rate(nq * len(e2e_s), world, e2e_t)
 
+    # ---- §8f-4 consumers of the same structure (reported beside the metric, not part of it):
+    # ball range search (count + fill + per-query sort) and the k-NN graph over every live point
+    extras = None
+    if not args.no_extras:
+        import math
+        nr = min(nq, 2_000_000)
+        unit_ball = math.pi ** (d / 2) / math.gamma(d / 2 + 1)
+        r2 = (10.0 / len(P) / unit_ball) ** (2.0 / d)  # ~10 points per query for uniform data
+        qr = Q_dev[:nr]
+        offs = torch.zeros(nr + 1, dtype=torch.int64, device=dev)
+        cap = 0
+        rng_ms = []
+        for rep in range(3):
+            if rep == 0:
+                cap = g.range_device(qr, r2, offs, None, None, 0)  # counts only: sizes the row buffers
+                rids = torch.empty(cap, dtype=torch.int32, device=dev)
+                rd2 = torch.empty(cap, dtype=torch.float64, device=dev)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            g.range_device(qr, r2, offs, rids, rd2, cap)
+            rng_ms.append(1000 * (time.perf_counter() - t0))
+        del rids, rd2, offs
+        live = g.info()["live"]
+        kg = 10
+        rows = torch.empty(live, dtype=torch.int32, device=dev)
+        gids = torch.empty((live, kg), dtype=torch.int32, device=dev)
+        gd2 = torch.empty((live, kg), dtype=torch.float64, device=dev)
+        gr_ms = []
+        for rep in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            g.knn_graph_device(kg, rows, gids, gd2)
+            gr_ms.append(1000 * (time.perf_counter() - t0))
+        del rows, gids, gd2
+        extras = {
+            "range_search": {"queries_per_s": nr / (min(rng_ms[1:]) / 1000.0), "ms": min(rng_ms[1:]), "queries": nr,
+                             "r2": r2, "rows": cap, "rows_per_query": cap / nr,
+                             "note": "ball range search through gk_bdl_range_device (count pass, scan, fill pass, "
+                                     "per-query (d2, id) sort), device-resident queries, best of 2 warm runs"},
+            "knn_graph": {"rows_per_s": live / (min(gr_ms[1:]) / 1000.0), "ms": min(gr_ms[1:]), "rows": live, "k": kg,
+                          "note": "gk_bdl_knn_graph_device over every live point (gather + id sort + kNN_L k+1 + "
+                                  "self drop), best of 2 warm runs"},
+        }
+
     if rank == 0:
         hbm, peak_src = measured_peaks()
         fp64_peak = measure_fp64_peak(dev)
@@ -343,6 +388,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": nq * k * (4 + 8)},
             "gpu_launches": 10 * args.steps,  # k_qbox_init, k_qbox, k_curve_key, 6 CUB radix-sort kernels, k_knn
             "clocks": clk.summary(),
+            "consumers": extras,
             "build": {"insert_l_points_per_s": len(P) / build_wall, "buildveb_points_per_s": built / (build_ms / 1000.0),
                       "insert_l_ms": 1000 * build_wall, "buildveb_ms": build_ms, "points": built,
                       "cold_insert_l_ms": 1000 * build_runs[0][0],

@@ -141,3 +141,58 @@ def test_knn_graph_device(gk, oracle):
     assert np.array_equal(rows.cpu().numpy().view(np.uint32), orr)
     assert np.array_equal(ids.cpu().numpy().view(np.uint32), oi)
     assert np.array_equal(d2.cpu().numpy(), od)
+
+
+@pytest.mark.slow
+def test_full_c2_range_sampled(gk, oracle):
+    """BASELINE config 2 structure (10M points): 2M ball queries with ~10 points each; every row
+    sorted by (d2, id) with d2 <= r2 recomputed from the coordinates, and exact oracle parity on
+    5k sampled queries."""
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(2)
+    P, Q = script[0][1], script[1][1][:2_000_000]
+    r2 = float((10.0 / len(P) / (4.0 / 3.0 * np.pi)) ** (2.0 / 3.0))
+    g = gk.BDLTree(3)
+    g.insert(P)
+    offs, ids, d2 = g.range(Q, r2)
+    assert offs[-1] == len(ids) and 5 < len(ids) / len(Q) < 15
+    q_of = np.repeat(np.arange(len(Q)), np.diff(offs).astype(np.int64))
+    t = Q[q_of] - P[ids]
+    rec = t[:, 0] * t[:, 0] + t[:, 1] * t[:, 1] + t[:, 2] * t[:, 2]
+    assert np.array_equal(rec, d2) and (d2 <= r2).all()
+    same_q = q_of[1:] == q_of[:-1]
+    assert ((d2[1:] > d2[:-1]) | ((d2[1:] == d2[:-1]) & (ids[1:] > ids[:-1])) | ~same_q).all()
+    o = oracle.BDLTree(3)
+    o.insert(P)
+    rows = np.random.default_rng(3).choice(len(Q), 5_000, replace=False)
+    oo, oi, od = o.range(Q[rows], r2)
+    assert np.array_equal(np.diff(offs)[rows], np.diff(oo))
+    got_i = np.concatenate([ids[offs[r]:offs[r + 1]] for r in rows])
+    got_d = np.concatenate([d2[offs[r]:offs[r + 1]] for r in rows])
+    assert np.array_equal(got_i, oi) and np.array_equal(got_d, od)
+
+
+@pytest.mark.slow
+def test_full_c5_knn_graph_sampled(gk, oracle):
+    """BASELINE config 5 (10M random-walk points, three 10 % Erase_L batches): the k-NN graph over the
+    surviving points; oracle parity (kNN_L with k + 1, self dropped) on 20k sampled rows."""
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(5)
+    g = gk.BDLTree(2)
+    o = oracle.BDLTree(2)
+    for op in script:
+        if op[0] == "insert":
+            g.insert(op[1]); o.insert(op[1])
+        elif op[0] == "erase":
+            assert g.erase(op[1]) == o.erase(op[1])
+    k = 10
+    rows, ids, d2 = g.knn_graph(k)
+    lid, lpts = o.live()
+    assert np.array_equal(rows, lid)
+    assert not (ids == rows[:, None]).any()
+    smp = np.random.default_rng(5).choice(len(rows), 20_000, replace=False)
+    oi, od = o.knn(lpts[smp], k + 1)
+    for j, r in enumerate(smp):
+        keep = oi[j] != rows[r]
+        want_i, want_d = oi[j][keep][:k], od[j][keep][:k]
+        assert np.array_equal(ids[r], want_i) and np.array_equal(d2[r], want_d), r
