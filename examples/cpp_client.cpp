@@ -18,7 +18,11 @@ int main() {
     for (auto& [d2, id] : row) std::printf("(%u, %.3g) ", id, d2);
     std::printf("\n");
   }
+  auto ball = tree.range(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 2), 1e-4);  // range search
+  std::printf("range rows %zu %zu\n", ball[0].size(), ball[1].size());
   const unsigned long long erased = tree.erase(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 10));
+  auto graph = tree.knn_graph(2);  // k-NN graph over the live points
+  std::printf("graph rows %zu, first row of id %u\n", graph.size(), graph[0].first);
   std::printf("erased %llu, live %llu\n", erased, (unsigned long long)tree.size());
   return 0;
 }

@@ -97,6 +97,41 @@ class BDLTree {
     detail::check(gk_bdl_knn(h_, queries, nq, k, ids, d2));
   }
 
+  /// Range search (ball): per query every live point with squared distance <= r2, sorted by
+  /// (sqdist, id) (the kd-tree range search of PAPER.md:188-190, 204).
+  template <class PointSet>
+  std::vector<std::vector<Entry>> range(const PointSet& S, double r2) {
+    const std::uint64_t nq = S.size();
+    std::vector<std::uint64_t> counts(nq), offs(nq + 1);
+    detail::check(gk_bdl_range_count(h_, detail::data_of(S), nq, r2, counts.data()));
+    std::uint64_t total = 0;
+    for (auto c : counts) total += c;
+    std::vector<PointId> ids(total ? total : 1);
+    std::vector<double> d2(total ? total : 1);
+    detail::check(gk_bdl_range(h_, detail::data_of(S), nq, r2, offs.data(), ids.data(), d2.data(), total));
+    std::vector<std::vector<Entry>> out(nq);
+    for (std::uint64_t i = 0; i < nq; ++i)
+      for (std::uint64_t j = offs[i]; j < offs[i + 1]; ++j) out[i].emplace_back(d2[j], ids[j]);
+    return out;
+  }
+
+  /// k-NN graph: for every live point (ascending id) its k nearest other
+  /// live points, sorted by (sqdist, id); returns (point id, neighbours) rows.
+  std::vector<std::pair<PointId, std::vector<Entry>>> knn_graph(int k) {
+    if (k < 1) throw std::invalid_argument("k must be >= 1");
+    const std::uint64_t n = size();
+    std::vector<PointId> rows(n), ids(n * k);
+    std::vector<double> d2(n * k);
+    detail::check(gk_bdl_knn_graph(h_, k, rows.data(), ids.data(), d2.data()));
+    std::vector<std::pair<PointId, std::vector<Entry>>> out(n);
+    for (std::uint64_t r = 0; r < n; ++r) {
+      out[r].first = rows[r];
+      for (int j = 0; j < k; ++j)
+        if (ids[r * k + j] != kNoPoint) out[r].second.emplace_back(d2[r * k + j], ids[r * k + j]);
+    }
+    return out;
+  }
+
   gk_bdl_info info() const {
     gk_bdl_info i;
     detail::check(gk_bdl_info_get(h_, &i));
