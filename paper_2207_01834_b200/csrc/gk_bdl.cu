@@ -758,20 +758,36 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
     if (nq == 0) return;
     DevScope ds(h->device);
     const TreeSet ts = h->trees();
-    // chunk schedule: n chunks growing geometrically by `ratio` (small first chunk -> the D2H link
-    // starts early; later chunks large -> compact query packets).  Tunable for experiments via
-    // GK_PIPE_CHUNKS / GK_PIPE_RATIO.
+    // chunk schedule (weights below); experiments: GK_PIPE_FRACS="w1,w2,..." or a geometric
+    // schedule of GK_PIPE_CHUNKS chunks growing by GK_PIPE_RATIO.
     int nchunk = 4;
     double ratio = 1.0;
     if (const char* e = std::getenv("GK_PIPE_CHUNKS")) nchunk = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("GK_PIPE_RATIO")) ratio = std::max(0.1, std::atof(e));
+    std::vector<double> wts;  // chunk weights: geometric, or an explicit list (GK_PIPE_FRACS="1,8,7,4,4")
+    if (const char* e = std::getenv("GK_PIPE_FRACS")) {
+      for (const char* p = e; *p;) {
+        char* end = nullptr;
+        const double v = std::strtod(p, &end);
+        if (end == p) break;
+        if (v > 0) wts.push_back(v);
+        p = (*end == ',') ? end + 1 : end;
+      }
+    }
+    if (wts.empty() && (std::getenv("GK_PIPE_CHUNKS") || std::getenv("GK_PIPE_RATIO")))
+      for (int c = 0; c < nchunk; ++c) wts.push_back(std::pow(ratio, c));
+    // default: two large chunks first (their packets stay compact: K1 of a 1/4 chunk costs 1.6x its
+    // share of the one-piece kernel), then shrinking ones so the last D2H after the last kNN_L is short.
+    // C2 sweep (profiles/e2e_sweep.py): 7,7,5,3,2 -> 29.9 ms; 4 equal chunks 31.1; 3 equal 30.6.
+    if (wts.empty()) wts = {7, 7, 5, 3, 2};
+    nchunk = static_cast<int>(wts.size());
     std::vector<std::uint64_t> bounds{0};
     {
-      double wsum = 0.0, w = 1.0;
-      for (int c = 0; c < nchunk; ++c, w *= ratio) wsum += w;
+      double wsum = 0.0;
+      for (double w : wts) wsum += w;
       double acc = 0.0;
-      w = 1.0;
-      for (int c = 0; c < nchunk; ++c, w *= ratio) {
+      for (int c = 0; c < nchunk; ++c) {
+        const double w = wts[c];
         acc += w;
         const std::uint64_t e = c + 1 == nchunk ? nq : static_cast<std::uint64_t>(static_cast<double>(nq) * acc / wsum);
         if (e - bounds.back() >= (1u << 16) || (c + 1 == nchunk && e > bounds.back())) bounds.push_back(e);

@@ -73,8 +73,12 @@ def main():
     ref_ids = None
     for spec in os.environ.get("SWEEP", "1 2 3 4 6 8").split():
         nc, _, r = spec.partition(":")
-        os.environ["GK_PIPE_CHUNKS"] = nc
-        os.environ["GK_PIPE_RATIO"] = r or "1"
+        if nc == "f":  # explicit chunk weights, e.g. f:1,8,7,4,4
+            os.environ["GK_PIPE_FRACS"] = r
+        else:
+            os.environ.pop("GK_PIPE_FRACS", None)
+            os.environ["GK_PIPE_CHUNKS"] = nc
+            os.environ["GK_PIPE_RATIO"] = r or "1"
         t = timeit(lambda: gk.lib().gk_bdl_knn(g._h, Qh.ctypes.data, nq, k, ids_h.ctypes.data, d2_h.ctypes.data))
         if ref_ids is None:
             ref_ids = ids_h.copy()
