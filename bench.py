@@ -248,6 +248,9 @@ def run_gpu(args):
         bms, built = g.last_build_ms()
         build_runs.append((wall, bms))
     build_wall = min(w for w, _ in build_runs[1:])
+    inf0 = g.info()
+    build_bytes = sum(max(0, int(inf0["height_per_tree"][i]) - 1) * int(inf0["build_size"][i])
+                      for i in range(64) if inf0["F"] >> i & 1) * (8 + 2 * (8 * d + 4))
     build_ms = min(b for _, b in build_runs[1:])
     del P_dev
 
@@ -351,13 +354,14 @@ def run_gpu(args):
         fp64_peak = measure_fp64_peak(dev)
         k1_ms = statistics.mean(trav_ms)
         achieved = bytes_per_q * nq / (k1_ms / 1000.0) / 1e9
-        traffic = None
+        traffic = issue_pct = None
         tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
         if os.path.exists(tp):
             try:
                 tj = json.load(open(tp))
                 if tj.get("config") == args.config:
                     traffic = tj.get("dram_bytes_per_launch")
+                    issue_pct = tj.get("issue_active_pct")
             except Exception:
                 traffic = None
         cpu = None
@@ -382,7 +386,10 @@ def run_gpu(args):
                          "fp64_peak_tflops": fp64_peak,
                          "fp64_frac": flops_per_q * nq / (k1_ms / 1000.0) / 1e12 / fp64_peak if fp64_peak else None,
                          "fp64_peak_source": "measured here: cuBLAS DGEMM 8192^3 via torch, best of 3",
-                         "counters": ctr},
+                         "counters": ctr,
+                         "issue_active_pct": issue_pct,
+                         "issue_note": "ncu smsp__issue_active of this kernel (profiles/k1_traffic.json): the "
+                                       "tree is L1/L2-resident, so K1 is bound by instruction issue, not DRAM"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 8,
                     "d2h_bytes_per_step": nq * k * (4 + 8)},
@@ -390,6 +397,11 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "consumers": extras,
             "build": {"insert_l_points_per_s": len(P) / build_wall, "buildveb_points_per_s": built / (build_ms / 1000.0),
+                      "hbm_frac": build_bytes / (build_ms / 1000.0) / 1e9 / hbm,
+                      "algorithmic_bytes": build_bytes,
+                      "bytes_note": "sum over trees of (height - 1) x n x (8 + 2 (8D + 4)) B: every point's split "
+                                    "coordinate read by the count pass and its coordinates + id read and written by "
+                                    "the partition at every level above its leaf; / build device time / HBM peak",
                       "insert_l_ms": 1000 * build_wall, "buildveb_ms": build_ms, "points": built,
                       "cold_insert_l_ms": 1000 * build_runs[0][0],
                       "note": "Insert_L of all points into a fresh handle (device-resident input, ingest+validation "

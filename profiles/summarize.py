@@ -46,13 +46,16 @@ def k1_tables(rep):
     traffic = float(m["dram__bytes_read.sum"][0]) * scale[m["dram__bytes_read.sum"][1]] + \
         float(m["dram__bytes_write.sum"][0]) * scale[m["dram__bytes_write.sum"][1]]
     ms = float(m["gpu__time_duration.sum"][0]) * {"ms": 1, "us": 1e-3, "ns": 1e-6}[m["gpu__time_duration.sum"][1]]
-    return "\n".join(k1), "\n".join(stt), traffic, ms
+    issue = float(m["smsp__issue_active.avg.pct_of_peak_sustained_active"][0])
+    inst = float(m["smsp__inst_executed.sum"][0])
+    return "\n".join(k1), "\n".join(stt), traffic, ms, issue, inst
 
 
 if __name__ == "__main__":
     lt, n = launch_table(sys.argv[1])
-    k1, st, traffic, ms = k1_tables(sys.argv[2])
+    k1, st, traffic, ms, issue, inst = k1_tables(sys.argv[2])
     json.dump({"config": 2, "kernel": "k_knn<3,10>", "dram_bytes_per_launch": traffic,
+               "issue_active_pct": issue, "warp_instructions": inst, "ncu_ms": ms,
                "source": "profiles/r1_summary.md (ncu --set full of the bench command)"},
               open(os.path.join(HERE, "k1_traffic.json"), "w"), indent=1)
     print(f"<!-- launches: {n} -->\n{lt}\n\n{k1}\n\n{st}\n\ntraffic {traffic / 1e9:.2f} GB, K1 {ms:.2f} ms")
