@@ -124,7 +124,11 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
   constexpr bool kPairMode = D >= 5;  // leaf work dominates at high D (C3: ~8x packet union)
   constexpr int kPairLanes = 10;      // <= this many needing lanes: pair-parallel leaf scan
-  __shared__ double s_q[kWarps][kPairMode ? D * 32 : 1];       // the tile's queries, [D][lane]
+#ifndef GK_PAIR_SMEM_Q
+#define GK_PAIR_SMEM_Q 0  // 1: the tile's queries in shared memory for the pair-parallel scan (else shuffles)
+#endif
+  constexpr bool kSmemQ = GK_PAIR_SMEM_Q != 0;
+  __shared__ double s_q[kWarps][(kPairMode && kSmemQ) ? D * 32 : 1];  // the tile's queries, [D][lane]
   __shared__ std::uint8_t s_own[kWarps][32];                   // lanes needing the current leaf
   // per-lane top-K heap, one column per thread (conflict-free): [K][blockDim] d2, then [K][blockDim] ids
   extern __shared__ double s_cand[];
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
     qhi[j] = __double2float_ru(q[j]);
     qlo2[j] = pk2(qlo[j], qlo[j]);
     qhi2[j] = pk2(qhi[j], qhi[j]);
-    if (kPairMode) s_q[w][j * 32 + lane] = q[j];
+    if (kPairMode && kSmemQ) s_q[w][j * 32 + lane] = q[j];
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) {
@@ -256,21 +260,34 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
           const std::uint32_t dqi = 32u / c, dp = 32u % c;
           std::uint32_t qi = static_cast<std::uint32_t>(lane) / c, pp = static_cast<std::uint32_t>(lane) % c;
           for (std::uint32_t t0 = 0; t0 < total; t0 += 32) {
-            int own = 0;
+            const bool valid = t0 + lane < total;
+            const int own = valid ? s_own[w][qi] : 0;
             double d2 = 0.0;
             bool cand = false;
-            if (t0 + lane < total) {
-              own = s_own[w][qi];
-              const double* qo = &s_q[w][own];
-              const double t = __dsub_rn(qo[0], s_pts[w][pp]);
+            if (kSmemQ) {
+              if (valid) {
+                const double* qo = &s_q[w][own];
+                const double t = __dsub_rn(qo[0], s_pts[w][pp]);
+                d2 = __dmul_rn(t, t);
+#pragma unroll
+                for (int j = 1; j < D; ++j) {
+                  const double tt = __dsub_rn(qo[j * 32], s_pts[w][j * GK_MAX_LEAF + pp]);
+                  d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
+                }
+              }
+            } else {
+              // the owner's query straight from its registers (keeps ~14 KB of shared memory per
+              // block free at D = 7: 4 blocks per SM instead of 3)
+              const std::uint32_t ppc = valid ? pp : 0u;
+              const double t = __dsub_rn(__shfl_sync(0xffffffffu, q[0], own), s_pts[w][ppc]);
               d2 = __dmul_rn(t, t);
 #pragma unroll
               for (int j = 1; j < D; ++j) {
-                const double tt = __dsub_rn(qo[j * 32], s_pts[w][j * GK_MAX_LEAF + pp]);
+                const double tt = __dsub_rn(__shfl_sync(0xffffffffu, q[j], own), s_pts[w][j * GK_MAX_LEAF + ppc]);
                 d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
               }
-              cand = d2 <= s_cand[w * 32 + own];  // owner's heap root = its k-th distance
             }
+            if (valid) cand = d2 <= s_cand[w * 32 + own];  // owner's heap root = its k-th distance
             unsigned bal = __ballot_sync(0xffffffffu, cand);
             while (bal) {
               const int b = __ffs(bal) - 1;
