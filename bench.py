@@ -309,10 +309,10 @@ def run_gpu(args):
     # ball range search (count + fill + per-query sort) and the k-NN graph over every live point
     extras = None
     if not args.no_extras:
-        import math
         nr = min(nq, 2_000_000)
-        unit_ball = math.pi ** (d / 2) / math.gamma(d / 2 + 1)
-        r2 = (10.0 / len(P) / unit_ball) ** (2.0 / d)  # ~10 points per query for uniform data
+        # radius: the median k-th neighbour distance of these queries (~k rows per query whatever the
+        # density; the kNN rows of the timed steps are still in d2_dev)
+        r2 = float(d2_dev[:nr, k - 1].median().item())
         qr = Q_dev[:nr]
         offs = torch.zeros(nr + 1, dtype=torch.int64, device=dev)
         cap = 0
@@ -341,7 +341,8 @@ def run_gpu(args):
         del rows, gids, gd2
         extras = {
             "range_search": {"queries_per_s": nr / (min(rng_ms[1:]) / 1000.0), "ms": min(rng_ms[1:]), "queries": nr,
-                             "r2": r2, "rows": cap, "rows_per_query": cap / nr,
+                             "r2": r2, "r2_rule": f"median {k}-th neighbour squared distance of the queries",
+                             "rows": cap, "rows_per_query": cap / nr,
                              "note": "ball range search through gk_bdl_range_device (count pass, scan, fill pass, "
                                      "per-query (d2, id) sort), device-resident queries, best of 2 warm runs"},
             "knn_graph": {"rows_per_s": live / (min(gr_ms[1:]) / 1000.0), "ms": min(gr_ms[1:]), "rows": live, "k": kg,

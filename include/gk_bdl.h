@@ -10,7 +10,7 @@
  *   gk_bdl_erase    <- bdl_erase (Erase_L)                   SPEC.md:581-589, PAPER.md:1255-1269 (Alg. 4)
  *   gk_bdl_knn      <- bdl_knn (kNN_L) over knn_batch/kNN_S
  *                      rows = KnnBuffer::extract() order     geokit/kdtree/knn_buffer.hpp:42-46 (sorted by (d2, id))
- *   gk_bdl_range    <- kd-tree range search (ball)           PAPER.md:188-190, 204, 230 (
+ *   gk_bdl_range    <- kd-tree range search (ball / box)     PAPER.md:188-190, 204, 230 (
  *                      SPEC.md:628 leaves it out of geokit's scope)
  *   gk_bdl_knn_graph <- k-NN graph generator over kNN
  *   point layout    <- Point<D>/PointSet<D>: D doubles, AoS  geokit/core/point.hpp:11-16
@@ -124,6 +124,15 @@ int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* o
                  uint64_t capacity);
 int gk_bdl_range_device(gk_bdl* h, const double* q_dev, uint64_t nq, double r2, uint64_t* offsets_dev, uint32_t* ids_dev,
                         double* d2_dev, uint64_t capacity, uint64_t* total);
+
+/* Orthogonal (box) range search: for every query box [lo_i, hi_i] (row-major nq x dim each), the
+ * ids of the live points p with lo_i[j] <= p[j] <= hi_i[j] for all j, ascending; offsets / capacity
+ * as for gk_bdl_range (an empty box, lo > hi in some j, has no rows). */
+int gk_bdl_range_box_count(gk_bdl* h, const double* lo, const double* hi, uint64_t nq, uint64_t* counts);
+int gk_bdl_range_box(gk_bdl* h, const double* lo, const double* hi, uint64_t nq, uint64_t* offsets, uint32_t* ids,
+                     uint64_t capacity);
+int gk_bdl_range_box_device(gk_bdl* h, const double* lo_dev, const double* hi_dev, uint64_t nq, uint64_t* offsets_dev,
+                            uint32_t* ids_dev, uint64_t capacity, uint64_t* total);
 
 /* k-NN graph (ParGeo's generator over kd-tree kNN): one row per live point in
  * ascending id order (row_ids[r] = its id; gk_bdl_info.live rows), holding its k nearest live

@@ -617,6 +617,26 @@ static void range_rec(const Tree& T, std::int32_t slot, const double* q, double 
   range_rec(T, nd.right, q, r2, out);
 }
 
+// Orthogonal range search over one tree: prune a subtree whose box misses [lo, hi]; report
+// live leaf points inside the closed box.
+static void range_box_rec(const Tree& T, std::int32_t slot, const double* lo, const double* hi, std::vector<Id>& out) {
+  const Node& nd = T.nodes[slot];
+  for (int j = 0; j < T.d; ++j)
+    if (nd.hi[j] < lo[j] || nd.lo[j] > hi[j]) return;
+  if (nd.kind == 1) {
+    for (std::uint32_t i = nd.start; i < nd.start + nd.count; ++i) {
+      if (T.dead[i]) continue;
+      const double* p = &T.pts[static_cast<std::size_t>(i) * T.d];
+      bool in = true;
+      for (int j = 0; j < T.d; ++j) in = in && lo[j] <= p[j] && p[j] <= hi[j];
+      if (in) out.push_back(T.ids[i]);
+    }
+    return;
+  }
+  range_box_rec(T, nd.left, lo, hi, out);
+  range_box_rec(T, nd.right, lo, hi, out);
+}
+
 // every live tree of the structure (order irrelevant: rows sorted by (d2, id))
 static void range_l(const Bdl& b, const double* Q, std::size_t nq, double r2,
                     std::vector<std::vector<std::pair<double, Id>>>& res) {
@@ -841,6 +861,32 @@ std::uint64_t gko_bdl_range(void* h, const double* Q, std::uint64_t nq, double r
     for (const auto& e : res[i]) {
       if (ids) ids[o] = e.second;
       if (d2) d2[o] = e.first;
+      ++o;
+    }
+  }
+  return o;
+}
+
+// orthogonal range search: counts (always) and, when ids is given, the rows (ascending ids)
+std::uint64_t gko_bdl_range_box(void* h, const double* LO, const double* HI, std::uint64_t nq, std::uint64_t* counts,
+                                std::uint32_t* ids) {
+  const Bdl& b = *static_cast<Bdl*>(h);
+  std::vector<const Tree*> trees;
+  for (int i = 63; i >= 0; --i)
+    if ((b.F >> i & 1ULL) && b.statics[i].live > 0) trees.push_back(&b.statics[i]);
+  if (b.buf_tree.live > 0) trees.push_back(&b.buf_tree);
+  std::vector<std::vector<Id>> res(nq);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(nq); ++i) {
+    for (const Tree* T : trees)
+      if (T->root >= 0 && T->live > 0) range_box_rec(*T, T->root, LO + i * b.d, HI + i * b.d, res[i]);
+    std::sort(res[i].begin(), res[i].end());
+  }
+  std::uint64_t o = 0;
+  for (std::size_t i = 0; i < nq; ++i) {
+    if (counts) counts[i] = res[i].size();
+    for (Id id : res[i]) {
+      if (ids) ids[o] = id;
       ++o;
     }
   }

@@ -93,6 +93,8 @@ def lib():
         L.gko_bdl_live.argtypes = [_P, _P, _P]
         L.gko_bdl_range.restype = _u64
         L.gko_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P]
+        L.gko_bdl_range_box.restype = _u64
+        L.gko_bdl_range_box.argtypes = [_P, _P, _P, _u64, _P, _P]
         L.gko_bdl_knn_graph.restype = _u64
         L.gko_bdl_knn_graph.argtypes = [_P, C.c_int, _P, _P, _P]
         L.gko_brute_knn.argtypes = [C.c_int, _P, _P, _u64, _P, _u64, C.c_int, _P, _P]
@@ -299,6 +301,18 @@ class BDLTree:
         offs = np.zeros(len(q) + 1, np.uint64)
         offs[1:] = np.cumsum(cnt)
         return offs, ids[:tot], d2[:tot]
+
+    def range_box(self, lo: np.ndarray, hi: np.ndarray):
+        """orthogonal range search: (offsets (n+1,), ids ascending per query)"""
+        lo = np.ascontiguousarray(lo, np.float64).reshape(-1, self.d)
+        hi = np.ascontiguousarray(hi, np.float64).reshape(-1, self.d)
+        cnt = np.zeros(len(lo), np.uint64)
+        tot = int(lib().gko_bdl_range_box(self.h, _ptr(lo), _ptr(hi), len(lo), _ptr(cnt), None))
+        ids = np.zeros(max(tot, 1), np.uint32)
+        lib().gko_bdl_range_box(self.h, _ptr(lo), _ptr(hi), len(lo), _ptr(cnt), _ptr(ids))
+        offs = np.zeros(len(lo) + 1, np.uint64)
+        offs[1:] = np.cumsum(cnt)
+        return offs, ids[:tot]
 
     def knn_graph(self, k: int):
         n = int(lib().gko_bdl_live(self.h, None, None))

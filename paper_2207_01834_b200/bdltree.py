@@ -79,6 +79,9 @@ def lib():
         L.gk_bdl_range_count.argtypes = [_P, _P, _u64, C.c_double, _P]
         L.gk_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64]
         L.gk_bdl_range_device.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64, C.POINTER(_u64)]
+        L.gk_bdl_range_box_count.argtypes = [_P, _P, _P, _u64, _P]
+        L.gk_bdl_range_box.argtypes = [_P, _P, _P, _u64, _P, _P, _u64]
+        L.gk_bdl_range_box_device.argtypes = [_P, _P, _P, _u64, _P, _P, _u64, C.POINTER(_u64)]
         L.gk_bdl_knn_graph.argtypes = [_P, C.c_int, _P, _P, _P]
         L.gk_bdl_knn_graph_device.argtypes = [_P, C.c_int, _P, _P, _P]
         L.gk_bdl_info_get.argtypes = [_P, C.POINTER(_Info)]
@@ -136,6 +139,7 @@ class BDLTree:
       knn(S, k)        kNN_L     (bdl_knn) -> (ids uint32 (n,k), sqdist float64 (n,k))
       range(S, r2)     range search (ball) -> (offsets uint64 (n+1,), ids, sqdist) rows sorted by (d2, id)
       range_count(S, r2) -> counts uint64 (n,)
+      range_box(lo, hi) orthogonal range search -> (offsets uint64 (n+1,), ids ascending)
       knn_graph(k)     k-NN graph -> (row ids (m,), ids (m,k), sqdist (m,k)), one row per live point
     Device variants take torch CUDA tensors and keep everything in HBM.
     """
@@ -202,6 +206,23 @@ class BDLTree:
         _check(lib().gk_bdl_range(self._h, _ptr(q), q.shape[0], float(r2), _ptr(offs), _ptr(ids), _ptr(d2), cap))
         return offs, ids[:cap], d2[:cap]
 
+    def range_box_count(self, lo, hi) -> np.ndarray:
+        lo, hi = _rows(lo, self.d), _rows(hi, self.d)
+        if lo.shape != hi.shape:
+            raise ValueError("lo and hi must have the same shape")
+        out = np.empty(lo.shape[0], np.uint64)
+        _check(lib().gk_bdl_range_box_count(self._h, _ptr(lo), _ptr(hi), lo.shape[0], _ptr(out)))
+        return out
+
+    def range_box(self, lo, hi):
+        """Orthogonal range search: ids of the live points in each closed box [lo, hi], ascending."""
+        lo, hi = _rows(lo, self.d), _rows(hi, self.d)
+        cap = int(self.range_box_count(lo, hi).sum()) if lo.shape[0] else 0
+        offs = np.zeros(lo.shape[0] + 1, np.uint64)
+        ids = np.empty(max(cap, 1), np.uint32)
+        _check(lib().gk_bdl_range_box(self._h, _ptr(lo), _ptr(hi), lo.shape[0], _ptr(offs), _ptr(ids), cap))
+        return offs, ids[:cap]
+
     def knn_graph(self, k: int):
         n = self.info()["live"]
         rows = np.empty(n, np.uint32)
@@ -233,6 +254,12 @@ class BDLTree:
         t = _u64(0)
         _check(lib().gk_bdl_range_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), float(r2), _ptr(offs_dev),
                                          _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
+        return int(t.value)
+
+    def range_box_device(self, lo_dev, hi_dev, offs_dev, ids_dev, capacity: int) -> int:
+        t = _u64(0)
+        _check(lib().gk_bdl_range_box_device(self._h, _ptr(lo_dev), _ptr(hi_dev), int(lo_dev.shape[0]), _ptr(offs_dev),
+                                             _ptr(ids_dev), int(capacity), C.byref(t)))
         return int(t.value)
 
     def knn_graph_device(self, k: int, rows_dev, ids_dev, d2_dev) -> None:

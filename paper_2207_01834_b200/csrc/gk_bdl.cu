@@ -972,6 +972,123 @@ int gk_bdl_range_device(gk_bdl* h, const double* q_dev, uint64_t nq, double r2, 
   });
 }
 
+// Orthogonal (box) range search: ids of the live points in the closed box [lo, hi], ascending.
+static std::uint64_t range_box_device_impl(gk_bdl* h, const double* lo, const double* hi, std::uint64_t nq,
+                                           unsigned long long* counts_dev, unsigned long long* offs_dev,
+                                           std::uint32_t* ids_dev, std::uint64_t capacity) {
+  if (nq >= 0x7fffffffULL) throw Error(GK_ERR_INVALID, "range batch larger than 2^31-1 queries");
+  if (nq == 0) {
+    if (offs_dev) GK_CUDA(cudaMemsetAsync(offs_dev, 0, 8, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    return 0;
+  }
+  const TreeSet ts = h->trees();
+  unsigned long long* cnt = counts_dev ? counts_dev : dalloc<unsigned long long>(nq + 1, h->st);
+  GK_CUDA(cudaMemsetAsync(cnt, 0, (nq + (counts_dev ? 0 : 1)) * 8, h->st));
+  std::uint32_t* perm = nullptr;
+  std::uint64_t total = 0;
+  if (ts.count > 0) {
+    perm = dalloc<std::uint32_t>(nq, h->st);
+    range_box_order(h->d, lo, hi, nq, perm, h->st);
+    range_box_launch(h->d, ts, lo, hi, nq, perm, cnt, nullptr, nullptr, false, h->st);
+  }
+  bool too_small = false;
+  if (offs_dev) {
+    std::size_t tb = 0;
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs_dev, nq + 1, h->st));
+    void* tmp = dalloc<char>(tb, h->st);
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs_dev, nq + 1, h->st));
+    dfree(tmp, h->st);
+    unsigned long long t = 0;
+    GK_CUDA(cudaMemcpyAsync(&t, offs_dev + nq, 8, cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    total = t;
+    if (ids_dev) {
+      if (total > capacity) too_small = true;
+      else if (total > 0) {
+        range_box_launch(h->d, ts, lo, hi, nq, perm, nullptr, offs_dev, ids_dev, true, h->st);
+        range_box_sort(ids_dev, total, offs_dev, nq, h->st);
+      }
+    }
+  }
+  if (perm) dfree(perm, h->st);
+  if (!counts_dev) dfree(cnt, h->st);
+  GK_CUDA(cudaStreamSynchronize(h->st));
+  if (too_small)
+    throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
+                                    std::to_string(capacity) + ")");
+  return total;
+}
+
+int gk_bdl_range_box_count(gk_bdl* h, const double* lo, const double* hi, uint64_t nq, uint64_t* counts) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(nq == 0 || (lo && hi && counts), "null buffer");
+    DevScope ds(h->device);
+    if (nq == 0) return;
+    double* dl = dalloc<double>(2 * nq * h->d, h->st);
+    double* dh = dl + nq * h->d;
+    unsigned long long* dc = dalloc<unsigned long long>(nq, h->st);
+    GK_CUDA(cudaMemcpyAsync(dl, lo, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    GK_CUDA(cudaMemcpyAsync(dh, hi, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    range_box_device_impl(h, dl, dh, nq, dc, nullptr, nullptr, 0);
+    GK_CUDA(cudaMemcpyAsync(counts, dc, nq * 8, cudaMemcpyDeviceToHost, h->st));
+    dfree(dl, h->st);
+    dfree(dc, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_range_box(gk_bdl* h, const double* lo, const double* hi, uint64_t nq, uint64_t* offsets, uint32_t* ids,
+                     uint64_t capacity) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(offsets != nullptr && (nq == 0 || (lo && hi)), "null buffer");
+    DevScope ds(h->device);
+    if (nq == 0) {
+      offsets[0] = 0;
+      return;
+    }
+    double* dl = dalloc<double>(2 * nq * h->d, h->st);
+    double* dh = dl + nq * h->d;
+    unsigned long long* doff = dalloc<unsigned long long>(nq + 1, h->st);
+    GK_CUDA(cudaMemcpyAsync(dl, lo, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    GK_CUDA(cudaMemcpyAsync(dh, hi, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    const std::uint64_t total = range_box_device_impl(h, dl, dh, nq, nullptr, doff, nullptr, 0);
+    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
+    GK_CUDA(cudaStreamSynchronize(h->st));
+    if (total > capacity) {
+      dfree(dl, h->st);
+      dfree(doff, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+      throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
+                                      std::to_string(capacity) + ")");
+    }
+    if (total > 0) {
+      need(ids != nullptr, "null row buffer");
+      std::uint32_t* di = dalloc<std::uint32_t>(total, h->st);
+      range_box_device_impl(h, dl, dh, nq, nullptr, doff, di, total);
+      GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
+      dfree(di, h->st);
+    }
+    dfree(dl, h->st);
+    dfree(doff, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_range_box_device(gk_bdl* h, const double* lo_dev, const double* hi_dev, uint64_t nq, uint64_t* offsets_dev,
+                            uint32_t* ids_dev, uint64_t capacity, uint64_t* total) {
+  return guard([&] {
+    need(h != nullptr && offsets_dev != nullptr, "null handle/offsets");
+    need(nq == 0 || (lo_dev && hi_dev), "null boxes");
+    DevScope ds(h->device);
+    const std::uint64_t t = range_box_device_impl(h, lo_dev, hi_dev, nq, nullptr,
+                                                  reinterpret_cast<unsigned long long*>(offsets_dev), ids_dev, capacity);
+    if (total) *total = t;
+  });
+}
+
 // ---------------------------------------------------------------- kNN graph --
 static void knn_graph_impl(gk_bdl* h, int k, std::uint32_t* row_ids_dev, std::uint32_t* ids_dev, double* d2_dev) {
   need(k >= 1, "k must be >= 1");

@@ -183,6 +183,13 @@ void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_
                   cudaStream_t st);
 void range_sort(std::uint32_t* ids, double* d2, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
                 cudaStream_t st);
+// orthogonal (box) range search: ids of live points in [lo, hi] per query, ascending
+void range_box_order(int d, const double* lo, const double* hi, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st);
+void range_box_launch(int d, const TreeSet& trees, const double* lo, const double* hi, std::uint64_t nq,
+                      const std::uint32_t* perm, unsigned long long* counts, const unsigned long long* offs,
+                      std::uint32_t* ids, bool fill, cudaStream_t st);
+void range_box_sort(std::uint32_t* ids, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
+                    cudaStream_t st);
 // kNN graph over the n live points of `trees`: rows in ascending id order (row_ids), k neighbours each
 void knn_graph_launch(int d, int k, const TreeSet& trees, std::uint64_t n, std::uint32_t* row_ids, std::uint32_t* ids,
                       double* d2, cudaStream_t st);

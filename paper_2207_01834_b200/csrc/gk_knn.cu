@@ -762,6 +762,148 @@ void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, un
   GK_CUDA(cudaFreeAsync(tile_ctr, st));
 }
 
+
+// ------------------------------------------------- range search (box) --
+// Orthogonal range search: every live point p with lo_j <= p_j <= hi_j for all j (closed
+// box).  Same packet traversal; a child is entered when any lane's query box meets the
+// child's fp32 box (both rounded outward: conservative), a staged point is reported when
+// it lies in the box in exact fp64 (NaN tombstones never do).  Queries ordered by the K2
+// key of their box centres.
+template <int D, bool FILL>
+__global__ void __launch_bounds__(256) k_range_box(const TreeSet ts, const double* __restrict__ LO,
+                                                   const double* __restrict__ HI, const std::uint32_t* __restrict__ perm,
+                                                   std::uint64_t nq, unsigned long long* __restrict__ counts,
+                                                   const unsigned long long* __restrict__ offs,
+                                                   std::uint32_t* __restrict__ out_ids, unsigned* __restrict__ tile_ctr) {
+  constexpr int kWarps = 8;
+  __shared__ std::uint64_t s_stack[kWarps][kStack];
+  __shared__ __align__(16) double s_pts[kWarps][D * GK_MAX_LEAF];
+  __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const unsigned ntiles = static_cast<unsigned>((nq + 31) / 32);
+  while (true) {
+    unsigned tile = 0;
+    if (lane == 0) tile = atomicAdd(tile_ctr, 1u);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= ntiles) break;
+    const std::uint64_t qi = static_cast<std::uint64_t>(tile) * 32 + lane;
+    const bool active = qi < nq;
+    std::uint32_t orig = 0;
+    double lo[D], hi[D];
+    float flo[D], fhi[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) { lo[j] = 1.0; hi[j] = -1.0; }  // inactive lanes: empty box
+    if (active) {
+      orig = perm[qi];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        lo[j] = LO[static_cast<std::uint64_t>(orig) * D + j];
+        hi[j] = HI[static_cast<std::uint64_t>(orig) * D + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      flo[j] = __double2float_rd(lo[j]);
+      fhi[j] = __double2float_ru(hi[j]);
+    }
+    unsigned long long cnt = 0;
+    const unsigned long long base = (FILL && active) ? offs[orig] : 0ULL;
+    for (int t = 0; t < ts.count; ++t) {
+      const float* __restrict__ nodes = static_cast<const float*>(ts.t[t].tnodes);
+      const double* __restrict__ coords = ts.t[t].coords;
+      const std::uint32_t* __restrict__ ids = ts.t[t].ids;
+      const std::uint64_t stride = ts.t[t].stride;
+      std::uint64_t ref = ts.t[t].root;
+      int sp = 0;
+      while (true) {
+        if (is_leaf_ref(ref)) {
+          const std::uint32_t c = leaf_count(ref);
+          const std::uint64_t s = leaf_start(ref);
+          __syncwarp();
+          if (lane < static_cast<int>(c)) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) s_pts[w][j * GK_MAX_LEAF + lane] = coords[j * stride + s + lane];
+            if (FILL) s_ids[w][lane] = ids[s + lane];
+          }
+          __syncwarp();
+          for (std::uint32_t p = 0; p < c; ++p) {
+            bool in = true;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              const double x = s_pts[w][j * GK_MAX_LEAF + p];
+              in = in && (lo[j] <= x) && (x <= hi[j]);
+            }
+            if (in) {
+              if (FILL) out_ids[base + cnt] = s_ids[w][p];
+              ++cnt;
+            }
+          }
+        } else {
+          const TNode<D>* nd = reinterpret_cast<const TNode<D>*>(nodes) + ref;
+          bool w0 = true, w1 = true;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const float2 l = *reinterpret_cast<const float2*>(nd->lo[j]);
+            const float2 h = *reinterpret_cast<const float2*>(nd->hi[j]);
+            w0 = w0 && l.x <= fhi[j] && h.x >= flo[j];
+            w1 = w1 && l.y <= fhi[j] && h.y >= flo[j];
+          }
+          w0 = w0 && active;
+          w1 = w1 && active;
+          const std::uint64_t r0 = nd->ref[0], r1 = nd->ref[1];
+          const unsigned b0 = __ballot_sync(0xffffffffu, w0), b1 = __ballot_sync(0xffffffffu, w1);
+          if (b0 && b1) {
+            if (lane == 0) s_stack[w][sp] = r1;
+            ++sp;
+            ref = r0;
+            continue;
+          } else if (b0) {
+            ref = r0;
+            continue;
+          } else if (b1) {
+            ref = r1;
+            continue;
+          }
+        }
+        __syncwarp();
+        if (sp == 0) break;
+        ref = s_stack[w][--sp];
+      }
+    }
+    if (active && !FILL) counts[orig] = cnt;
+  }
+}
+
+__global__ void k_box_centre(const double* __restrict__ lo, const double* __restrict__ hi, std::uint64_t n,
+                             double* __restrict__ c) {
+  const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) c[i] = 0.5 * lo[i] + 0.5 * hi[i];  // finite for any finite box
+}
+
+template <int D>
+void range_box_d(const TreeSet& ts, const double* lo, const double* hi, std::uint64_t nq, unsigned long long* counts,
+                 const unsigned long long* offs, std::uint32_t* ids, bool fill, const std::uint32_t* perm, cudaStream_t st) {
+  static int grid = 0;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    int dev = 0, sms = 0, per0 = 0, per1 = 0;
+    GK_CUDA(cudaGetDevice(&dev));
+    GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k_range_box<D, false>, 256, 0));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_range_box<D, true>, 256, 0));
+    grid = std::max(1, std::min(per0, per1)) * sms;
+  });
+  const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(grid, (nq + 255) / 256));
+  unsigned* tile_ctr = nullptr;
+  GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
+  GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
+  if (fill) k_range_box<D, true><<<g, 256, 0, st>>>(ts, lo, hi, perm, nq, counts, offs, ids, tile_ctr);
+  else k_range_box<D, false><<<g, 256, 0, st>>>(ts, lo, hi, perm, nq, counts, offs, ids, tile_ctr);
+  GK_CHECK_LAUNCH();
+  GK_CUDA(cudaFreeAsync(tile_ctr, st));
+}
+
 }  // namespace
 
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq, std::uint32_t* ids_dev,
@@ -899,6 +1041,46 @@ void knn_graph_launch(int d, int k, const TreeSet& ts, std::uint64_t n, std::uin
   GK_CUDA(cudaFreeAsync(q, st));
   GK_CUDA(cudaFreeAsync(ti, st));
   GK_CUDA(cudaFreeAsync(td, st));
+}
+
+void range_box_order(int d, const double* lo, const double* hi, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st) {
+  double* c = nullptr;
+  GK_CUDA(cudaMallocAsync(&c, nq * d * 8, st));
+  k_box_centre<<<static_cast<unsigned>((nq * d + 255) / 256), 256, 0, st>>>(lo, hi, nq * d, c);
+  GK_CHECK_LAUNCH();
+  range_order(d, c, nq, perm, st);
+  GK_CUDA(cudaFreeAsync(c, st));
+}
+
+void range_box_launch(int d, const TreeSet& trees, const double* lo, const double* hi, std::uint64_t nq,
+                      const std::uint32_t* perm, unsigned long long* counts, const unsigned long long* offs,
+                      std::uint32_t* ids, bool fill, cudaStream_t st) {
+  if (nq == 0) return;
+  switch (d) {
+#define GK_D(DD) case DD: range_box_d<DD>(trees, lo, hi, nq, counts, offs, ids, fill, perm, st); break;
+    GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+// each query's rows in ascending id order
+void range_box_sort(std::uint32_t* ids, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
+                    cudaStream_t st) {
+  if (total == 0) return;
+  if (total > 0x7fffffffULL || nq > 0x7fffffffULL)
+    throw Error(GK_ERR_UNSUPPORTED, "range result larger than 2^31-1 rows");
+  std::uint32_t* ids2 = nullptr;
+  GK_CUDA(cudaMallocAsync(&ids2, total * 4, st));
+  const int ni = static_cast<int>(total), ns = static_cast<int>(nq);
+  std::size_t tb = 0;
+  GK_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, ids, ids2, ni, ns, offs, offs + 1, st));
+  void* tmp = nullptr;
+  GK_CUDA(cudaMallocAsync(&tmp, tb, st));
+  GK_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, tb, ids, ids2, ni, ns, offs, offs + 1, st));
+  GK_CUDA(cudaMemcpyAsync(ids, ids2, total * 4, cudaMemcpyDeviceToDevice, st));
+  GK_CUDA(cudaFreeAsync(tmp, st));
+  GK_CUDA(cudaFreeAsync(ids2, st));
 }
 
 }  // namespace gk

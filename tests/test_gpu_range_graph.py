@@ -196,3 +196,42 @@ def test_full_c5_knn_graph_sampled(gk, oracle):
         keep = oi[j] != rows[r]
         want_i, want_d = oi[j][keep][:k], od[j][keep][:k]
         assert np.array_equal(ids[r], want_i) and np.array_equal(d2[r], want_d), r
+
+
+@pytest.mark.parametrize("d", [2, 3, 7])
+def test_range_box_parity(gk, oracle, d):
+    rng = np.random.default_rng(300 + d)
+    g, o = _pair(gk, oracle, d, X=256, leaf=8)
+    P = rng.random((20_000, d))
+    P[15_000:15_500] = P[:500]
+    for part in np.array_split(P, 3):
+        g.insert(part); o.insert(part)
+    E = P[rng.choice(len(P), 2_000, replace=False)]
+    assert g.erase(E) == o.erase(E)
+    c = np.concatenate([rng.random((3_000, d)), P[:500]])
+    for half in (0.0, 0.02, 0.15):
+        lo, hi = c - half, c + half * rng.random((len(c), d))  # asymmetric boxes
+        go, gi = g.range_box(lo, hi)
+        oo, oi = o.range_box(lo, hi)
+        assert np.array_equal(go, oo) and np.array_equal(gi, oi), (d, half)
+        assert np.array_equal(g.range_box_count(lo, hi), np.diff(oo))
+    go, gi = g.range_box(c + 0.1, c - 0.1)  # empty boxes
+    assert not go.any() and len(gi) == 0
+
+
+def test_range_box_device(gk, oracle):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(17)
+    g, o = _pair(gk, oracle, 3)
+    P = rng.random((50_000, 3))
+    g.insert(P); o.insert(P)
+    c = rng.random((10_000, 3))
+    lo, hi = c - 0.01, c + 0.01
+    oo, oi = o.range_box(lo, hi)
+    total = int(oo[-1])
+    offs = torch.zeros(len(c) + 1, dtype=torch.int64, device="cuda")
+    ids = torch.zeros(max(total, 1), dtype=torch.int32, device="cuda")
+    t = g.range_box_device(torch.from_numpy(lo).cuda(), torch.from_numpy(hi).cuda(), offs, ids, total)
+    assert t == total
+    assert np.array_equal(offs.cpu().numpy().view(np.uint64), oo)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32)[:total], oi)

@@ -260,3 +260,18 @@ def test_knn_graph_oracle_vs_brute(oracle, k):  # PAPER.md:202-203 (k-NN graph g
         want_d = dd[keep][order]
         assert np.array_equal(ids[r, :len(want_i)], want_i), r
         assert np.array_equal(d2[r, :len(want_d)], want_d), r
+
+
+@pytest.mark.parametrize("d", [2, 3, 6])
+def test_range_box_oracle_vs_brute(oracle, d):  # orthogonal kd-tree range search
+    o, rng = _small_structure(oracle, d, 31 + d)
+    ids_live, P = o.live()
+    c = np.concatenate([rng.random((50, d)), P[:10]])
+    for half in (0.0, 0.05, 0.3, 2.0):
+        lo, hi = c - half, c + half
+        offs, ids = o.range_box(lo, hi)
+        for i in range(len(c)):
+            m = ((P >= lo[i]) & (P <= hi[i])).all(1)
+            assert np.array_equal(ids[offs[i]:offs[i + 1]], np.sort(ids_live[m])), (half, i)
+    offs, ids = o.range_box(c + 0.1, c - 0.1)  # empty boxes
+    assert len(ids) == 0
