@@ -200,11 +200,12 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
 // GK_TRACE=1: host-side phase timestamps of Insert_L on stderr (diagnostics only)
 struct PhaseTrace {
   bool on = std::getenv("GK_TRACE") != nullptr;
+  bool nosync = on && std::getenv("GK_TRACE")[0] == '2';  // GK_TRACE=2: host stamps only, no stream syncs
   cudaStream_t st = nullptr;  // synchronised before each stamp when tracing
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   void operator()(const char* what, long long arg = -1) const {
     if (!on) return;
-    if (st) GK_CUDA(cudaStreamSynchronize(st));
+    if (st && !nosync) GK_CUDA(cudaStreamSynchronize(st));
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     std::fprintf(stderr, "[gk] %8.3f ms  %s %lld\n", ms, what, arg);
   }
