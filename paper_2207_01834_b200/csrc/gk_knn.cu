@@ -567,9 +567,13 @@ void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, c
   GK_CHECK_LAUNCH();
   void* tmp = nullptr;
   std::size_t tb = 0;
-  GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, perm_out, static_cast<int>(nq), 0, bits, st));
-  GK_CUDA(cudaMallocAsync(&tmp, tb, st));
-  GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, perm_out, static_cast<int>(nq), 0, bits, st));
+  auto sort = [&](auto n) {  // 32-bit item counts when they fit (CUB's faster offset type), else 64-bit
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, perm_out, n, 0, bits, st));
+    GK_CUDA(cudaMallocAsync(&tmp, tb, st));
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, perm_out, n, 0, bits, st));
+  };
+  if (nq <= 0x7fffffffULL) sort(static_cast<int>(nq));
+  else sort(static_cast<long long>(nq));
   GK_CUDA(cudaFreeAsync(tmp, st));
   GK_CUDA(cudaFreeAsync(box, st));
   GK_CUDA(cudaFreeAsync(keys, st));
@@ -1002,7 +1006,7 @@ void range_sort(std::uint32_t* ids, double* d2, std::uint64_t total, const unsig
 void knn_graph_launch(int d, int k, const TreeSet& ts, std::uint64_t n, std::uint32_t* row_ids, std::uint32_t* ids,
                       double* d2, cudaStream_t st) {
   if (n == 0) return;
-  if (n >= 0xffffffffULL) throw Error(GK_ERR_INVALID, "kNN graph over more than 2^32-1 points");
+  if (n > 0x7fffffffULL) throw Error(GK_ERR_UNSUPPORTED, "kNN graph over more than 2^31-1 points");
   double *pts = nullptr, *q = nullptr, *td = nullptr;
   std::uint32_t *uid = nullptr, *pos = nullptr, *src = nullptr, *ti = nullptr;
   unsigned long long* ctr = nullptr;

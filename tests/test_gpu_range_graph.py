@@ -235,3 +235,30 @@ def test_range_box_device(gk, oracle):
     assert t == total
     assert np.array_equal(offs.cpu().numpy().view(np.uint64), oo)
     assert np.array_equal(ids.cpu().numpy().view(np.uint32)[:total], oi)
+
+
+@pytest.mark.slow
+def test_knn_batch_beyond_2_31_queries(gk, oracle):
+    """Maximum batch size: one kNN_L call with 2^31 + 2^20 queries (the K2 sort takes 64-bit item
+    counts past 2^31); sampled rows exact against the oracle."""
+    torch = pytest.importorskip("torch")
+    free, _ = torch.cuda.mem_get_info()
+    nq = (1 << 31) + (1 << 20)
+    if free < nq * (16 + 8 + 4 + 8) * 1.3:
+        pytest.skip("needs ~100 GB of free HBM")
+    rng = np.random.default_rng(77)
+    P = rng.random((200_000, 2))
+    g = gk.BDLTree(2)
+    g.insert(P)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    Q = torch.rand((nq, 2), dtype=torch.float64, device="cuda", generator=gen)
+    ids = torch.empty((nq, 1), dtype=torch.int32, device="cuda")
+    d2 = torch.empty((nq, 1), dtype=torch.float64, device="cuda")
+    g.knn_device(Q, 1, ids, d2)
+    rows = torch.from_numpy(np.concatenate([rng.integers(0, nq, 3000), [0, nq - 1, (1 << 31) - 1, 1 << 31]])).cuda()
+    q = Q[rows].cpu().numpy()
+    o = oracle.BDLTree(2)
+    o.insert(P)
+    oi, od = o.knn(q, 1)
+    assert np.array_equal(ids[rows].cpu().numpy().view(np.uint32), oi)
+    assert np.array_equal(d2[rows].cpu().numpy(), od)
