@@ -926,6 +926,7 @@ int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* o
   return guard([&] {
     need(h != nullptr, "null handle");
     need(offsets != nullptr && (nq == 0 || q), "null buffer");
+    need(capacity == 0 || (ids && d2), "null row buffers");
     DevScope ds(h->device);
     if (nq == 0) {
       offsets[0] = 0;
@@ -933,31 +934,30 @@ int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* o
     }
     double* dq = dalloc<double>(nq * h->d, h->st);
     unsigned long long* doff = dalloc<unsigned long long>(nq + 1, h->st);
+    std::uint32_t* di = dalloc<std::uint32_t>(std::max<std::uint64_t>(capacity, 1), h->st);
+    double* dd = dalloc<double>(std::max<std::uint64_t>(capacity, 1), h->st);
     GK_CUDA(cudaMemcpyAsync(dq, q, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
-    // count pass first: the rows go to device buffers of exactly the total size
-    const std::uint64_t total = range_device_impl(h, dq, nq, r2, nullptr, doff, nullptr, nullptr, 0);
-    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
-    GK_CUDA(cudaStreamSynchronize(h->st));
-    if (total > capacity) {
+    auto release = [&] {
       dfree(dq, h->st);
       dfree(doff, h->st);
-      GK_CUDA(cudaStreamSynchronize(h->st));
-      throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
-                                      std::to_string(capacity) + ")");
-    }
-    if (total > 0) {
-      need(ids && d2, "null row buffers");
-      std::uint32_t* di = dalloc<std::uint32_t>(total, h->st);
-      double* dd = dalloc<double>(total, h->st);
-      range_device_impl(h, dq, nq, r2, nullptr, doff, di, dd, total);
-      GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
-      GK_CUDA(cudaMemcpyAsync(d2, dd, total * 8, cudaMemcpyDeviceToHost, h->st));
       dfree(di, h->st);
       dfree(dd, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+    };
+    std::uint64_t total = 0;
+    try {  // one count pass, one fill pass into the caller-sized row buffers
+      total = range_device_impl(h, dq, nq, r2, nullptr, doff, di, dd, capacity);
+    } catch (...) {
+      cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);  // offsets even when the rows do not fit
+      release();
+      throw;
     }
-    dfree(dq, h->st);
-    dfree(doff, h->st);
-    GK_CUDA(cudaStreamSynchronize(h->st));
+    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
+    if (total) {
+      GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
+      GK_CUDA(cudaMemcpyAsync(d2, dd, total * 8, cudaMemcpyDeviceToHost, h->st));
+    }
+    release();
   });
 }
 
@@ -1045,6 +1045,7 @@ int gk_bdl_range_box(gk_bdl* h, const double* lo, const double* hi, uint64_t nq,
   return guard([&] {
     need(h != nullptr, "null handle");
     need(offsets != nullptr && (nq == 0 || (lo && hi)), "null buffer");
+    need(capacity == 0 || ids, "null row buffer");
     DevScope ds(h->device);
     if (nq == 0) {
       offsets[0] = 0;
@@ -1053,28 +1054,26 @@ int gk_bdl_range_box(gk_bdl* h, const double* lo, const double* hi, uint64_t nq,
     double* dl = dalloc<double>(2 * nq * h->d, h->st);
     double* dh = dl + nq * h->d;
     unsigned long long* doff = dalloc<unsigned long long>(nq + 1, h->st);
+    std::uint32_t* di = dalloc<std::uint32_t>(std::max<std::uint64_t>(capacity, 1), h->st);
     GK_CUDA(cudaMemcpyAsync(dl, lo, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
     GK_CUDA(cudaMemcpyAsync(dh, hi, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
-    const std::uint64_t total = range_box_device_impl(h, dl, dh, nq, nullptr, doff, nullptr, 0);
-    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
-    GK_CUDA(cudaStreamSynchronize(h->st));
-    if (total > capacity) {
+    auto release = [&] {
       dfree(dl, h->st);
       dfree(doff, h->st);
-      GK_CUDA(cudaStreamSynchronize(h->st));
-      throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
-                                      std::to_string(capacity) + ")");
-    }
-    if (total > 0) {
-      need(ids != nullptr, "null row buffer");
-      std::uint32_t* di = dalloc<std::uint32_t>(total, h->st);
-      range_box_device_impl(h, dl, dh, nq, nullptr, doff, di, total);
-      GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
       dfree(di, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+    };
+    std::uint64_t total = 0;
+    try {  // one count pass, one fill pass into the caller-sized row buffer
+      total = range_box_device_impl(h, dl, dh, nq, nullptr, doff, di, capacity);
+    } catch (...) {
+      cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);  // offsets even when the rows do not fit
+      release();
+      throw;
     }
-    dfree(dl, h->st);
-    dfree(doff, h->st);
-    GK_CUDA(cudaStreamSynchronize(h->st));
+    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
+    if (total) GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
+    release();
   });
 }
 
