@@ -819,6 +819,10 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   }
 
   GK_TL_PRINT(level0);
+#if GK_BUILD_TIMELINE
+  unsigned long long tv_a = 0, tv_b = 0;
+  if (gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv_a));
+#endif
   // ---- vEB slots, top-down.  Depth d is the cut depth of exactly one frame
   // (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
   // pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees
@@ -872,6 +876,12 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     if (g == N) a.int_by_slot[N] = 0;
     else a.int_by_slot[__ldcg(&na.pos[g])] = (__ldcg(&na.flags[g]) & F_LEAF) ? 0u : 1u;
   }
+#if GK_BUILD_TIMELINE
+  if (gtid == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv_b));
+    printf("[tlveb] n=%u grid=%u H=%d N=%u vEB %.1f us\n", n, gridDim.x, H, N, (tv_b - tv_a) * 1e-3);
+  }
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::uint32_t* irank_by_slot) {
