@@ -229,6 +229,8 @@ struct gk_bdl {
   std::uint32_t* buf_src = nullptr;  // buffer-tree position -> arrival index
   std::uint64_t next_id = 0;
   float knn_ms = 0.f, knn_total_ms = 0.f, build_ms = 0.f;
+  double knn_ns_q = 0.0;  // device ns per query of the last one-shot kNN_L (k = knn_ns_k): e2e chunk planning
+  int knn_ns_k = 0;
   std::uint64_t built_pts = 0;
   void* cub_tmp = nullptr;
   std::size_t cub_bytes = 0;
@@ -719,6 +721,10 @@ static void knn_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, in
   GK_CUDA(cudaStreamSynchronize(h->st));
   GK_CUDA(cudaEventElapsedTime(&h->knn_ms, h->ev[2], h->ev[3]));
   GK_CUDA(cudaEventElapsedTime(&h->knn_total_ms, h->ev[0], h->ev[1]));
+  if (nq >= (1u << 16) && !ctr) {
+    h->knn_ns_q = 1e6 * h->knn_total_ms / static_cast<double>(nq);
+    h->knn_ns_k = k;
+  }
 }
 
 int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev) {
@@ -780,7 +786,19 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
     // default: two large chunks first (their packets stay compact: K1 of a 1/4 chunk costs 1.6x its
     // share of the one-piece kernel), then shrinking ones so the last D2H after the last kNN_L is short.
     // C2 sweep (profiles/e2e_sweep.py): 7,7,5,3,2 -> 29.9 ms; 4 equal chunks 31.1; 3 equal 30.6.
-    if (wts.empty()) wts = {7, 7, 5, 3, 2};
+    if (wts.empty()) {
+      // Chunking overlaps the PCIe copies with kNN_L but makes each chunk's query packets sparser
+      // (C2: a quarter of the queries costs 1.6x its share).  Plan from the device cost per query
+      // of the last one-shot kNN_L with this k (or a guess by dimension) against the PCIe cost:
+      //   compute-bound (C3, 7D: 25 ns vs 2.2 ns)  -> one coherent chunk (5 chunks were 1.6x slower);
+      //   transfer-bound, small batch (C1, 1M)     -> two chunks;
+      //   transfer-bound, large batch (C2, 10M)    -> 7,7,5,3,2 (two large chunks, short D2H tail).
+      const double tx = static_cast<double>(h->d * 8 + k * 12) / 55.0;  // ns per query at ~55 GB/s
+      const double tc = (h->knn_ns_k == k && h->knn_ns_q > 0.0) ? h->knn_ns_q : (h->d >= 5 ? 10.0 * tx : 0.5 * tx);
+      if (tc > 1.2 * tx) wts = {1};
+      else if (nq < (4ULL << 20)) wts = {1, 1};
+      else wts = {7, 7, 5, 3, 2};
+    }
     nchunk = static_cast<int>(wts.size());
     std::vector<std::uint64_t> bounds{0};
     {

@@ -29,7 +29,7 @@ def timeit(fn, reps=3):
 
 
 def main():
-    d, script = configs.make_inputs(2, 1.0)
+    d, script = configs.make_inputs(int(os.environ.get("CONFIG", "2")), 1.0)
     P = [op[1] for op in script if op[0] == "insert"][0]
     Q, k = [op for op in script if op[0] == "knn"][0][1:]
     nq = len(Q)
