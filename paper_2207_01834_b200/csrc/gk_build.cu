@@ -79,7 +79,11 @@ constexpr std::uint64_t kChunksPerWarp = GK_CHUNKS_PER_WARP;
 #ifndef GK_GROUP8_CHUNKS
 #define GK_GROUP8_CHUNKS 40
 #endif
-constexpr std::uint32_t kGroup16Chunks = GK_GROUP16_CHUNKS, kGroup8Chunks = GK_GROUP8_CHUNKS;
+#ifndef GK_GROUP4_CHUNKS
+#define GK_GROUP4_CHUNKS 80
+#endif
+constexpr std::uint32_t kGroup16Chunks = GK_GROUP16_CHUNKS, kGroup8Chunks = GK_GROUP8_CHUNKS,
+                        kGroup4Chunks = GK_GROUP4_CHUNKS;
 
 __host__ __device__ inline std::uint64_t hyperceiling_u(std::uint64_t x) {
   std::uint64_t p = 1;
@@ -609,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     // Sparse levels (many small chunks per warp): the warp splits into 32/gl lane groups that
     // partition as many chunks side by side, so the chunks' dependent metadata loads and their
     // point loads overlap instead of running one chunk after another
-    const std::uint32_t gl = cpw >= kGroup8Chunks ? 8u : (cpw >= kGroup16Chunks ? 16u : 32u);
+    const std::uint32_t gl =
+        cpw >= kGroup4Chunks ? 4u : (cpw >= kGroup8Chunks ? 8u : (cpw >= kGroup16Chunks ? 16u : 32u));
     if (PH == 1 && gl < 32) {
       const std::uint32_t ngr = 32 / gl, grp = lane / gl, gla = lane % gl;
       const unsigned gmask = ((1u << gl) - 1u) << (grp * gl);
@@ -696,19 +701,20 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
             mxr[j] = fmax(mxr[j], __shfl_xor_sync(0xffffffffu, mxr[j], o));
           }
         }
-        if (part && gla < 2 * D) {
-          const int j = static_cast<int>(gla) % D, side = static_cast<int>(gla) / D;
-          double l = side ? mnr[0] : mnl[0], h = side ? mxr[0] : mxl[0];
+        if (part)
+          for (int t = static_cast<int>(gla); t < 2 * D; t += static_cast<int>(gl)) {  // (side, dim) per lane
+            const int j = t % D, side = t / D;
+            double l = side ? mnr[0] : mnl[0], h = side ? mxr[0] : mxl[0];
 #pragma unroll
-          for (int jj = 1; jj < D; ++jj)
-            if (j == jj) { l = side ? mnr[jj] : mnl[jj]; h = side ? mxr[jj] : mxl[jj]; }
-          if (side ? nright_chunk : nleft_chunk) {
-            const std::uint64_t u = 2ULL * __ldcg(&a.irank[v]) + side;
-            unsigned long long* kk = a.keys + (u * D + j) * 2;
-            atomicMin(kk, dkey(l));
-            atomicMax(kk + 1, dkey(h));
+            for (int jj = 1; jj < D; ++jj)
+              if (j == jj) { l = side ? mnr[jj] : mnl[jj]; h = side ? mxr[jj] : mxl[jj]; }
+            if (side ? nright_chunk : nleft_chunk) {
+              const std::uint64_t u = 2ULL * __ldcg(&a.irank[v]) + side;
+              unsigned long long* kk = a.keys + (u * D + j) * 2;
+              atomicMin(kk, dkey(l));
+              atomicMax(kk + 1, dkey(h));
+            }
           }
-        }
       }
     } else
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
