@@ -141,15 +141,17 @@ __global__ void k_bloom_query(const std::uint64_t* __restrict__ bits, std::uint6
 // tombstones coordinate-exact matches with a CAS on coordinate 0 (so every
 // tombstone is counted once even with duplicate batch points).
 template <int D>
-__global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* __restrict__ P, std::uint64_t n,
+__global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* __restrict__ P,
+                                               const std::uint32_t* __restrict__ perm, std::uint64_t n,
                                                unsigned long long* killed) {
-  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
+  const std::uint64_t src = perm ? perm[i] : i;  // K2 (Hilbert) order: neighbouring threads walk neighbouring paths
   double p[D];
   float pf_lo[D], pf_hi[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    p[j] = P[i * D + j];
+    p[j] = P[src * D + j];
     pf_lo[j] = __double2float_rd(p[j]);
     pf_hi[j] = __double2float_ru(p[j]);
   }
@@ -452,23 +454,33 @@ struct gk_bdl {
     if (ts.count == 0) return 0;
     unsigned long long* killed = dalloc<unsigned long long>(kMaxTrees, st);
     GK_CUDA(cudaMemsetAsync(killed, 0, kMaxTrees * 8, st));
+    std::uint32_t* perm = nullptr;
+    if (n >= 4096 && n < 0xffffffffULL) {
+      perm = dalloc<std::uint32_t>(n, st);
+      range_order(d, P_aos, n, perm, st);
+    }
     switch (d) {
-#define GK_D(DD) case DD: k_erase<DD><<<blocks_for(n, 128), 128, 0, st>>>(ts, P_aos, n, killed); break;
+#define GK_D(DD) case DD: k_erase<DD><<<blocks_for(n, 128), 128, 0, st>>>(ts, P_aos, perm, n, killed); break;
       GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
 #undef GK_D
     }
     GK_CHECK_LAUNCH();
+    if (perm) dfree(perm, st);
     std::vector<unsigned long long> hk(kMaxTrees);
     GK_CUDA(cudaMemcpyAsync(hk.data(), killed, kMaxTrees * 8, cudaMemcpyDeviceToHost, st));
     GK_CUDA(cudaStreamSynchronize(st));
     dfree(killed, st);
     std::uint64_t total = 0;
+    std::vector<DevTree*> hit;
+    for (std::size_t t = 0; t < which.size(); ++t)
+      if (which[t] >= 0 && hk[t]) hit.push_back(&statics[which[t]]);
+    for (std::size_t t = 0; t < which.size(); ++t)
+      if (which[t] >= 0) statics[which[t]].live -= hk[t];
+    collapse_trees(d, hit, st);
     for (std::size_t t = 0; t < which.size(); ++t) {
       total += hk[t];
       if (which[t] >= 0) {
-        DevTree& T = statics[which[t]];
-        T.live -= hk[t];
-        if (hk[t]) collapse_tree(d, T, st);
+        continue;
       } else if (hk[t]) {
         // drop the dead buffer points, keeping arrival order, and rebuild the buffer tree
         std::uint32_t* flags = dalloc<std::uint32_t>(buf_n + 1, st);

@@ -1038,6 +1038,31 @@ void collapse_d(DevTree& T, cudaStream_t st) {
   dfree(arrive, st);
 }
 
+// the surviving root of a collapsed tree: {root slot, leaf?, start, count, internal rank}
+__global__ void k_root_info(const std::int32_t* __restrict__ repl, const gk_canon_node* __restrict__ canon,
+                            const std::uint32_t* __restrict__ irank, std::uint32_t* out) {
+  const std::int32_t r = repl[0];
+  out[0] = static_cast<std::uint32_t>(r);
+  if (r >= 0) {
+    out[1] = static_cast<std::uint32_t>(canon[r].kind);
+    out[2] = canon[r].start;
+    out[3] = canon[r].count;
+    out[4] = irank[r];
+  }
+}
+
+template <int D>
+void collapse_launch(DevTree& T, std::int32_t*& repl, std::uint32_t*& arrive, std::uint32_t* info, cudaStream_t st) {
+  const std::uint32_t N = static_cast<std::uint32_t>(T.n_nodes);
+  repl = dalloc<std::int32_t>(N, st);
+  arrive = dalloc<std::uint32_t>(N, st);
+  GK_CUDA(cudaMemsetAsync(arrive, 0, static_cast<std::size_t>(N) * 4, st));
+  k_collapse_up<<<blocks_for(N), 256, 0, st>>>(N, T.canon, T.coords, T.orig, repl, arrive);
+  k_relink<D><<<blocks_for(N), 256, 0, st>>>(N, T.canon, static_cast<TNode<D>*>(T.tnodes), T.irank, T.orig, repl);
+  k_root_info<<<1, 1, 0, st>>>(repl, T.canon, T.irank, info);
+  GK_CHECK_LAUNCH();
+}
+
 // ------------------------------------------------------------------ driver --
 int coresident_blocks(const void* fn) {
   int dev = 0, sms = 0, per = 0;
@@ -1269,6 +1294,38 @@ void collapse_tree(int d, DevTree& t, cudaStream_t st) {
     case 8: collapse_d<8>(t, st); break;
     default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
   }
+}
+
+// Erase_S collapses of several trees with one host round-trip for all their new roots
+void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st) {
+  std::vector<DevTree*> ts;
+  for (DevTree* t : trees)
+    if (t->n_nodes) ts.push_back(t);
+  if (ts.empty()) return;
+  const std::size_t m = ts.size();
+  std::uint32_t* info = dalloc<std::uint32_t>(5 * m, st);
+  std::vector<std::int32_t*> repl(m);
+  std::vector<std::uint32_t*> arrive(m);
+  for (std::size_t i = 0; i < m; ++i) {
+    switch (d) {
+#define GK_D(DD) case DD: collapse_launch<DD>(*ts[i], repl[i], arrive[i], info + 5 * i, st); break;
+      GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+      default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+    }
+  }
+  std::vector<std::uint32_t> h(5 * m);
+  GK_CUDA(cudaMemcpyAsync(h.data(), info, 5 * m * 4, cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  for (std::size_t i = 0; i < m; ++i) {
+    DevTree& T = *ts[i];
+    const std::int32_t root = static_cast<std::int32_t>(h[5 * i]);
+    T.root_slot = root;
+    if (root >= 0) T.root_ref = h[5 * i + 1] == 1 ? make_leaf_ref(h[5 * i + 2], h[5 * i + 3]) : h[5 * i + 4];
+    dfree(repl[i], st);
+    dfree(arrive[i], st);
+  }
+  dfree(info, st);
 }
 
 void free_tree(DevTree& t, cudaStream_t st) {

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/gk_bdl.h"
 
@@ -171,6 +172,8 @@ void free_tree(DevTree& t, cudaStream_t st);
 // and splice out internal nodes left with one child; relinks the canonical
 // nodes and the traversal nodes and updates root_slot / root_ref.
 void collapse_tree(int d, DevTree& t, cudaStream_t st);
+// the same for several trees, one host round-trip for all their new roots
+void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st);
 
 // knn.cu
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq,
