@@ -882,7 +882,13 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
 }
 
 // ------------------------------------------------------------ range search --
-// Ball range search over the log structure: counts, then rows.
+// Ball range search over the log structure.  Rows requested: one
+// traversal writes each query's first kRangeSlots rows into fixed slots and counts them all;
+// after the offset scan the slots are compacted into the CSR rows and only the queries with
+// more rows than slots are traversed again (their rows straight to their offsets).  Counts
+// only (or a slot buffer that would exceed kRangeSlotBytes): a count traversal.
+constexpr unsigned kRangeSlots = 16;
+constexpr std::uint64_t kRangeSlotBytes = 4ULL << 30;
 static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, double r2,
                                        unsigned long long* counts_dev, unsigned long long* offs_dev, std::uint32_t* ids_dev,
                                        double* d2_dev, std::uint64_t capacity) {
@@ -893,15 +899,33 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
     GK_CUDA(cudaStreamSynchronize(h->st));
     return 0;
   }
+  const bool rows = offs_dev && (ids_dev || d2_dev);
+  if (rows) need(ids_dev && d2_dev, "range rows need both ids and d2");
   const TreeSet ts = h->trees();
   unsigned long long* cnt = counts_dev ? counts_dev : dalloc<unsigned long long>(nq + 1, h->st);
   GK_CUDA(cudaMemsetAsync(cnt, 0, (nq + (counts_dev ? 0 : 1)) * 8, h->st));
   std::uint32_t* perm = nullptr;
+  std::uint32_t* ti = nullptr;
+  double* td = nullptr;
+  const bool slots = rows && nq * kRangeSlots * 12 <= kRangeSlotBytes;
   std::uint64_t total = 0;
+  auto release = [&] {
+    if (perm) dfree(perm, h->st);
+    if (ti) dfree(ti, h->st);
+    if (td) dfree(td, h->st);
+    if (!counts_dev) dfree(cnt, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  };
   if (ts.count > 0) {
     perm = dalloc<std::uint32_t>(nq, h->st);
     range_order(h->d, q_dev, nq, perm, h->st);
-    range_launch(h->d, ts, q_dev, nq, r2, perm, cnt, nullptr, nullptr, nullptr, false, h->st);
+    if (slots) {
+      ti = dalloc<std::uint32_t>(nq * kRangeSlots, h->st);
+      td = dalloc<double>(nq * kRangeSlots, h->st);
+      range_launch(h->d, ts, q_dev, nq, r2, perm, cnt, nullptr, ti, td, 2, kRangeSlots, h->st);
+    } else {
+      range_launch(h->d, ts, q_dev, nq, r2, perm, cnt, nullptr, nullptr, nullptr, 0, 0, h->st);
+    }
   }
   if (offs_dev) {
     std::size_t tb = 0;
@@ -913,24 +937,28 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
     GK_CUDA(cudaMemcpyAsync(&t, offs_dev + nq, 8, cudaMemcpyDeviceToHost, h->st));
     GK_CUDA(cudaStreamSynchronize(h->st));
     total = t;
-    if (ids_dev || d2_dev) {
+    if (rows) {
       if (total > capacity) {
-        if (perm) dfree(perm, h->st);
-        if (!counts_dev) dfree(cnt, h->st);
-        GK_CUDA(cudaStreamSynchronize(h->st));
+        release();
         throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
                                         std::to_string(capacity) + ")");
       }
-      need(ids_dev && d2_dev, "range rows need both ids and d2");
       if (total > 0) {
-        range_launch(h->d, ts, q_dev, nq, r2, perm, nullptr, offs_dev, ids_dev, d2_dev, true, h->st);
+        if (slots) {
+          std::uint32_t* ovf = dalloc<std::uint32_t>(nq, h->st);
+          const std::uint64_t no =
+              range_slots_compact(nq, kRangeSlots, perm, cnt, offs_dev, ti, td, ids_dev, d2_dev, ovf, h->st);
+          if (no)  // the overflowing queries again (in K2 order), rows straight to their offsets
+            range_launch(h->d, ts, q_dev, no, r2, ovf, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
+          dfree(ovf, h->st);
+        } else {
+          range_launch(h->d, ts, q_dev, nq, r2, perm, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
+        }
         range_sort(ids_dev, d2_dev, total, offs_dev, nq, h->st);
       }
     }
   }
-  if (perm) dfree(perm, h->st);
-  if (!counts_dev) dfree(cnt, h->st);
-  GK_CUDA(cudaStreamSynchronize(h->st));
+  release();
   return total;
 }
 

@@ -181,9 +181,14 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
                 cudaEvent_t ev_k0, cudaEvent_t ev_k1);
 // range search (ball, d2 <= r2): K2 order, count / fill passes over the same order, per-query sort
 void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st);
+// mode 0: counts; 1: rows at offs; 2: the first capq rows of query i at ids/d2 + i * capq, and counts
 void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const std::uint32_t* perm,
-                  unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, bool fill,
-                  cudaStream_t st);
+                  unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, int mode,
+                  unsigned capq, cudaStream_t st);
+// slot rows into CSR; returns the number of overflowing queries, listed in K2 order in ovf
+std::uint64_t range_slots_compact(std::uint64_t nq, unsigned capq, const std::uint32_t* perm,
+                                  const unsigned long long* counts, const unsigned long long* offs, const std::uint32_t* ti,
+                                  const double* td, std::uint32_t* ids, double* d2, std::uint32_t* ovf, cudaStream_t st);
 void range_sort(std::uint32_t* ids, double* d2, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
                 cudaStream_t st);
 // orthogonal (box) range search: ids of live points in [lo, hi] per query, ascending

@@ -633,13 +633,14 @@ __global__ void k_drop_self(std::uint64_t n, int k, const std::uint32_t* __restr
 // fp32 box lower bound is <= r2 rounded up (conservative), a staged leaf point is
 // reported when its exact fp64 d2 <= r2.  FILL = false counts per query, FILL = true
 // writes each query's rows at its offset (traversal order; sorted afterwards).
-template <int D, bool FILL>
+template <int D, int MODE>
 __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* __restrict__ Q,
                                                const std::uint32_t* __restrict__ perm, std::uint64_t nq, double r2,
                                                unsigned long long* __restrict__ counts,
                                                const unsigned long long* __restrict__ offs,
                                                std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
-                                               unsigned* __restrict__ tile_ctr) {
+                                               unsigned* __restrict__ tile_ctr, unsigned capq) {
+  constexpr bool FILL = MODE == 1, SLOTS = MODE == 2;  // 0: count; 1: rows at offs; 2: first capq rows + count
   constexpr int kWarps = 8;
   __shared__ std::uint64_t s_stack[kWarps][kStack];
   __shared__ __align__(16) double s_pts[kWarps][D * GK_MAX_LEAF];
@@ -673,7 +674,8 @@ __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* _
     const float rf = active ? __double2float_ru(r2) : -1.f;
     const double rq = active ? r2 : -1.0;
     unsigned long long cnt = 0;
-    const unsigned long long base = (FILL && active) ? offs[orig] : 0ULL;
+    const unsigned long long base =
+        (FILL && active) ? offs[orig] : (SLOTS ? static_cast<unsigned long long>(orig) * capq : 0ULL);
     for (int t = 0; t < ts.count; ++t) {
       const float4* __restrict__ nodes = static_cast<const float4*>(ts.t[t].tnodes);
       const double* __restrict__ coords = ts.t[t].coords;
@@ -689,7 +691,7 @@ __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* _
           if (lane < static_cast<int>(c)) {
 #pragma unroll
             for (int j = 0; j < D; ++j) s_pts[w][j * GK_MAX_LEAF + lane] = coords[j * stride + s + lane];
-            if (FILL) s_ids[w][lane] = ids[s + lane];
+            if (FILL || SLOTS) s_ids[w][lane] = ids[s + lane];
           }
           __syncwarp();
           for (std::uint32_t p = 0; p < c; ++p) {
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* _
               d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
             }
             if (d2 <= rq) {  // NaN (tombstone) never qualifies
-              if (FILL) {
+              if (FILL || (SLOTS && cnt < capq)) {
                 out_ids[base + cnt] = s_ids[w][p];
                 out_d2[base + cnt] = d2;
               }
@@ -745,25 +747,46 @@ __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* _
 
 template <int D>
 void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, unsigned long long* counts,
-             unsigned long long* offs, std::uint32_t* ids, double* d2, bool fill, std::uint32_t* perm, cudaStream_t st) {
+             unsigned long long* offs, std::uint32_t* ids, double* d2, int mode, unsigned capq, std::uint32_t* perm,
+             cudaStream_t st) {
   static int grid = 0;
   static std::once_flag once;
   std::call_once(once, [&] {
-    int dev = 0, sms = 0, per0 = 0, per1 = 0;
+    int dev = 0, sms = 0, per0 = 0, per1 = 0, per2 = 0;
     GK_CUDA(cudaGetDevice(&dev));
     GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k_range<D, false>, 256, 0));
-    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_range<D, true>, 256, 0));
-    grid = std::max(1, std::min(per0, per1)) * sms;
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k_range<D, 0>, 256, 0));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_range<D, 1>, 256, 0));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_range<D, 2>, 256, 0));
+    grid = std::max(1, std::min(per0, std::min(per1, per2))) * sms;
   });
   const unsigned g = static_cast<unsigned>(std::min<std::uint64_t>(grid, (nq + 255) / 256));
   unsigned* tile_ctr = nullptr;
   GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
   GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
-  if (fill) k_range<D, true><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr);
-  else k_range<D, false><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr);
+  if (mode == 1) k_range<D, 1><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr, capq);
+  else if (mode == 2) k_range<D, 2><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr, capq);
+  else k_range<D, 0><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr, capq);
   GK_CHECK_LAUNCH();
   GK_CUDA(cudaFreeAsync(tile_ctr, st));
+}
+
+// rows of the bounded-slot pass into their CSR place; flags (in K2 order) the queries with more
+// rows than slots, so that the list of those keeps the order's packet coherence
+__global__ void k_slots_compact(std::uint64_t nq, unsigned capq, const std::uint32_t* __restrict__ perm,
+                                const unsigned long long* __restrict__ counts, const unsigned long long* __restrict__ offs,
+                                const std::uint32_t* __restrict__ ti, const double* __restrict__ td,
+                                std::uint32_t* __restrict__ ids, double* __restrict__ d2, std::uint8_t* __restrict__ flag) {
+  const std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nq) return;
+  const std::uint32_t q = perm[i];
+  const unsigned long long c = counts[q], o = offs[q];
+  const unsigned m = static_cast<unsigned>(c < capq ? c : capq);
+  for (unsigned j = 0; j < m; ++j) {
+    ids[o + j] = ti[static_cast<std::uint64_t>(q) * capq + j];
+    d2[o + j] = td[static_cast<std::uint64_t>(q) * capq + j];
+  }
+  flag[i] = c > capq ? 1 : 0;
 }
 
 
@@ -961,19 +984,43 @@ void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* pe
 }
 
 void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const std::uint32_t* perm,
-                  unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, bool fill,
-                  cudaStream_t st) {
+                  unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, int mode,
+                  unsigned capq, cudaStream_t st) {
   if (nq == 0) return;
   switch (d) {
 #define GK_D(DD)                                                                                                \
   case DD:                                                                                                      \
-    range_d<DD>(trees, q_dev, nq, r2, counts, const_cast<unsigned long long*>(offs), ids, d2, fill,            \
+    range_d<DD>(trees, q_dev, nq, r2, counts, const_cast<unsigned long long*>(offs), ids, d2, mode, capq,      \
                 const_cast<std::uint32_t*>(perm), st);                                                          \
     break;
     GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
 #undef GK_D
     default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
   }
+}
+
+std::uint64_t range_slots_compact(std::uint64_t nq, unsigned capq, const std::uint32_t* perm,
+                                  const unsigned long long* counts, const unsigned long long* offs, const std::uint32_t* ti,
+                                  const double* td, std::uint32_t* ids, double* d2, std::uint32_t* ovf, cudaStream_t st) {
+  std::uint8_t* flag = nullptr;
+  unsigned long long* nsel = nullptr;
+  GK_CUDA(cudaMallocAsync(&flag, nq, st));
+  GK_CUDA(cudaMallocAsync(&nsel, 8, st));
+  k_slots_compact<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(nq, capq, perm, counts, offs, ti, td, ids, d2,
+                                                                         flag);
+  GK_CHECK_LAUNCH();
+  std::size_t tb = 0;
+  void* tmp = nullptr;
+  GK_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, perm, flag, ovf, nsel, static_cast<long long>(nq), st));
+  GK_CUDA(cudaMallocAsync(&tmp, tb, st));
+  GK_CUDA(cub::DeviceSelect::Flagged(tmp, tb, perm, flag, ovf, nsel, static_cast<long long>(nq), st));
+  unsigned long long h = 0;
+  GK_CUDA(cudaMemcpyAsync(&h, nsel, 8, cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  GK_CUDA(cudaFreeAsync(tmp, st));
+  GK_CUDA(cudaFreeAsync(flag, st));
+  GK_CUDA(cudaFreeAsync(nsel, st));
+  return h;
 }
 
 // Each query's rows sorted by (d2, id): an id sort, then a stable d2 sort, per segment.
