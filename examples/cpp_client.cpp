@@ -20,6 +20,8 @@ int main() {
   }
   auto ball = tree.range(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 2), 1e-4);  // range search
   std::printf("range rows %zu %zu\n", ball[0].size(), ball[1].size());
+  std::vector<std::array<double, 3>> lo{{0.4, 0.4, 0.4}}, hi{{0.45, 0.45, 0.45}};
+  std::printf("box rows %zu\n", tree.range_box(lo, hi)[0].size());  // orthogonal range search
   const unsigned long long erased = tree.erase(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 10));
   auto graph = tree.knn_graph(2);  // k-NN graph over the live points
   std::printf("graph rows %zu, first row of id %u\n", graph.size(), graph[0].first);

@@ -115,6 +115,22 @@ class BDLTree {
     return out;
   }
 
+  /// Orthogonal range search: per query box [lo_i, hi_i] the ids of the live points inside, ascending.
+  template <class PointSet>
+  std::vector<std::vector<PointId>> range_box(const PointSet& lo, const PointSet& hi) {
+    if (lo.size() != hi.size()) throw std::invalid_argument("lo and hi must hold the same number of boxes");
+    const std::uint64_t nq = lo.size();
+    std::vector<std::uint64_t> counts(nq), offs(nq + 1);
+    detail::check(gk_bdl_range_box_count(h_, detail::data_of(lo), detail::data_of(hi), nq, counts.data()));
+    std::uint64_t total = 0;
+    for (auto c : counts) total += c;
+    std::vector<PointId> ids(total ? total : 1);
+    detail::check(gk_bdl_range_box(h_, detail::data_of(lo), detail::data_of(hi), nq, offs.data(), ids.data(), total));
+    std::vector<std::vector<PointId>> out(nq);
+    for (std::uint64_t i = 0; i < nq; ++i) out[i].assign(ids.begin() + offs[i], ids.begin() + offs[i + 1]);
+    return out;
+  }
+
   /// k-NN graph: for every live point (ascending id) its k nearest other
   /// live points, sorted by (sqdist, id); returns (point id, neighbours) rows.
   std::vector<std::pair<PointId, std::vector<Entry>>> knn_graph(int k) {
