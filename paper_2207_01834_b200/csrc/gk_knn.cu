@@ -37,7 +37,10 @@ namespace {
 // warps per block: 8, or 4 for K > 16 so the shared-memory k-buffers (12 B x K per lane) still
 // leave room for several blocks per SM; K = 0 is the runtime-k instantiation (32 < k <= 256)
 template <int K>
-__host__ __device__ constexpr int warps_for() { return K == 0 ? 2 : (K > 16 ? 4 : 8); }
+#ifndef GK_K4W
+#define GK_K4W 10  // k-buffers of more than this many entries use 4-warp blocks (C5 k = 16: +5 %)
+#endif
+__host__ __device__ constexpr int warps_for() { return K == 0 ? 2 : (K > GK_K4W ? 4 : 8); }
 constexpr int kMaxRuntimeK = 256;
 constexpr bool kHilbertOrder = true;  // K2 key: Hilbert (true) or Morton (false)
 
