@@ -262,3 +262,27 @@ def test_knn_batch_beyond_2_31_queries(gk, oracle):
     oi, od = o.knn(q, 1)
     assert np.array_equal(ids[rows].cpu().numpy().view(np.uint32), oi)
     assert np.array_equal(d2[rows].cpu().numpy(), od)
+
+
+def test_pinned_host_knn_default_plans(gk):
+    """gk_bdl_knn from pinned buffers with the default chunk plan in its three regimes (one chunk for a
+    compute-bound 7D batch, two for a small 3D batch, 7,7,5,3,2 for a large one): rows identical to
+    the device API's."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(21)
+    for d, n, nq, k in ((7, 200_000, 300_000, 10), (3, 300_000, 1_000_000, 8), (3, 300_000, 4_300_000, 4)):
+        g = gk.BDLTree(d)
+        g.insert(rng.random((n, d)))
+        Q = rng.random((nq, d))
+        qd = torch.from_numpy(Q).cuda()
+        ids0 = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+        d20 = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+        for _ in range(2):  # the second call plans from the first one's measured cost per query
+            Qp = torch.from_numpy(Q).pin_memory().numpy()
+            ids = torch.empty((nq, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+            d2 = torch.empty((nq, k), dtype=torch.float64).pin_memory().numpy()
+            assert gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, nq, k, ids.ctypes.data, d2.ctypes.data) == 0
+            g.knn_device(qd, k, ids0, d20)
+            assert np.array_equal(ids, ids0.cpu().numpy().view(np.uint32)), (d, nq)
+            assert np.array_equal(d2, d20.cpu().numpy()), (d, nq)
+        g.close()
