@@ -50,7 +50,7 @@ enum gk_status {
 
 enum gk_heuristic { GK_SPATIAL_MEDIAN = 0, GK_OBJECT_MEDIAN = 1 }; /* PAPER.md:1484-1487 */
 
-#define GK_MAX_K 256
+#define GK_MAX_K 65536 /* k <= 256: k-buffers in shared memory; above: a global scratch heap */
 #define GK_MAX_LEAF 32
 
 typedef struct gk_bdl gk_bdl; /* opaque handle: owns all device arenas + one CUDA stream */
@@ -105,7 +105,7 @@ int gk_bdl_insert_device(gk_bdl* h, const double* pts_dev, uint64_t n);
 int gk_bdl_erase(gk_bdl* h, const double* pts, uint64_t n, uint64_t* n_erased);
 int gk_bdl_erase_device(gk_bdl* h, const double* pts_dev, uint64_t n, uint64_t* n_erased);
 
-/* kNN_L: exact k nearest live points of every query, 1 <= k <= GK_MAX_K (256). */
+/* kNN_L: exact k nearest live points of every query, 1 <= k <= GK_MAX_K. */
 int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, double* d2);
 int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev);
 /* Instrumented kNN_L (same results) that also counts the work of §8(d). */
@@ -136,7 +136,7 @@ int gk_bdl_range_box_device(gk_bdl* h, const double* lo_dev, const double* hi_de
 
 /* k-NN graph (ParGeo's generator over kd-tree kNN): one row per live point in
  * ascending id order (row_ids[r] = its id; gk_bdl_info.live rows), holding its k nearest live
- * points other than itself, sorted by (d2, id), padded with (GK_NO_POINT, +inf).  1 <= k <= 255. */
+ * points other than itself, sorted by (d2, id), padded with (GK_NO_POINT, +inf).  1 <= k < GK_MAX_K. */
 int gk_bdl_knn_graph(gk_bdl* h, int k, uint32_t* row_ids, uint32_t* ids, double* d2);
 int gk_bdl_knn_graph_device(gk_bdl* h, int k, uint32_t* row_ids_dev, uint32_t* ids_dev, double* d2_dev);
 

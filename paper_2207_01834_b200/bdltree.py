@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GK_LIB") or os.path.join(HERE, "_lib", "libgkbdl.so")
 
 NO_POINT = 0xFFFFFFFF  # geokit::core::kNoPoint
-MAX_K = 256
+MAX_K = 65536  # GK_MAX_K
 SPATIAL_MEDIAN, OBJECT_MEDIAN = 0, 1
 
 CANON_NODE = np.dtype([

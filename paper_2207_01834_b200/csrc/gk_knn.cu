@@ -40,7 +40,7 @@ template <int K>
 #ifndef GK_K4W
 #define GK_K4W 10  // k-buffers of more than this many entries use 4-warp blocks (C5 k = 16: +5 %)
 #endif
-__host__ __device__ constexpr int warps_for() { return K == 0 ? 2 : (K > GK_K4W ? 4 : 8); }
+__host__ __device__ constexpr int warps_for() { return K <= 0 ? 2 : (K > GK_K4W ? 4 : 8); }
 constexpr int kMaxRuntimeK = 256;
 constexpr bool kHilbertOrder = true;  // K2 key: Hilbert (true) or Morton (false)
 
@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
                                                         const std::uint32_t* __restrict__ perm, std::uint64_t nq, int k,
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
                                                         unsigned long long* __restrict__ counters,
-                                                        unsigned* __restrict__ tile_ctr) {
+                                                        unsigned* __restrict__ tile_ctr,
+                                                        double* __restrict__ gheap) {
   constexpr int kWarps = warps_for<KT>();
   const int K = KT > 0 ? KT : k;  // k-buffer size (compile-time for the common k)
   __shared__ std::uint64_t s_stack[kWarps][kStack];
@@ -134,10 +135,17 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   __shared__ double s_q[kWarps][(kPairMode && kSmemQ) ? D * 32 : 1];  // the tile's queries, [D][lane]
   __shared__ std::uint8_t s_own[kWarps][32];                   // lanes needing the current leaf
   // per-lane top-K heap, one column per thread (conflict-free): [K][blockDim] d2, then [K][blockDim] ids
+  // (KT < 0, k > kMaxRuntimeK: the same columns in a global scratch heap, one per resident thread,
+  // column stride = the grid's thread count; L1/L2 serve it)
   extern __shared__ double s_cand[];
-  double* cdv = s_cand + threadIdx.x;
-  std::uint32_t* civ = reinterpret_cast<std::uint32_t*>(s_cand + K * kWarps * 32) + threadIdx.x;
-  constexpr int CS = kWarps * 32;  // column stride
+  constexpr bool kGlobalHeap = KT < 0;
+  using CsT = std::conditional_t<kGlobalHeap, std::uint64_t, int>;
+  const CsT CS = kGlobalHeap ? static_cast<CsT>(gridDim.x) * blockDim.x : static_cast<CsT>(kWarps * 32);  // column stride
+  const std::uint64_t boff = kGlobalHeap ? static_cast<std::uint64_t>(blockIdx.x) * blockDim.x : 0;
+  double* hbase = kGlobalHeap ? gheap : s_cand;
+  double* cbase = hbase + boff;  // this block's columns
+  double* cdv = cbase + threadIdx.x;
+  std::uint32_t* civ = reinterpret_cast<std::uint32_t*>(hbase + K * CS) + boff + threadIdx.x;
 
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
                 d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
               }
             }
-            if (valid) cand = d2 <= s_cand[w * 32 + own];  // owner's heap root = its k-th distance
+            if (valid) cand = d2 <= cbase[w * 32 + own];  // owner's heap root = its k-th distance
             unsigned bal = __ballot_sync(0xffffffffu, cand);
             while (bal) {
               const int b = __ffs(bal) - 1;
@@ -514,8 +522,9 @@ void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std
               double* d2, unsigned long long* ctr, cudaStream_t st) {
   constexpr int kWarps = warps_for<KT>();
   const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
-  const int smem = (KT > 0 ? KT : k) * kWarps * 32 * 12;        // per-lane top-K columns
-  const int smem_max = (KT > 0 ? KT : kMaxRuntimeK) * kWarps * 32 * 12;
+  // per-lane top-K columns in shared memory (KT < 0: in a global scratch heap instead)
+  const int smem = KT < 0 ? 0 : (KT > 0 ? KT : k) * kWarps * 32 * 12;
+  const int smem_max = KT < 0 ? 0 : (KT > 0 ? KT : kMaxRuntimeK) * kWarps * 32 * 12;
   static std::once_flag once;             // per (D, K) instantiation
   static int sm_count = 0;
   std::call_once(once, [&] {
@@ -529,13 +538,22 @@ void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std
   int per = 0;  // resident blocks at this launch's shared-memory size
   GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn<D, KT, false>, kWarps * 32, smem));
   const int resident = std::max(1, per) * sm_count;
-  const unsigned grid = std::min<unsigned>(blocks, static_cast<unsigned>(resident));
+  unsigned grid = std::min<unsigned>(blocks, static_cast<unsigned>(resident));
+  double* gheap = nullptr;
+  if (KT < 0) {
+    // scratch heap of 12 k bytes per resident thread, bounded to ~4 GB (at least one block per SM)
+    const std::uint64_t per_block = static_cast<std::uint64_t>(kWarps) * 32 * k * 12;
+    const std::uint64_t cap = std::max<std::uint64_t>(sm_count, (4ull << 30) / per_block);
+    grid = static_cast<unsigned>(std::min<std::uint64_t>(grid, cap));
+    GK_CUDA(cudaMallocAsync(&gheap, per_block * grid, st));
+  }
   unsigned* tile_ctr = nullptr;
   GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
   GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
-  if (ctr) k_knn<D, KT, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
-  else k_knn<D, KT, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr);
+  if (ctr) k_knn<D, KT, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr, gheap);
+  else k_knn<D, KT, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr, gheap);
   GK_CUDA(cudaFreeAsync(tile_ctr, st));
+  if (gheap) GK_CUDA(cudaFreeAsync(gheap, st));
 }
 
 template <int D>
@@ -549,7 +567,8 @@ void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* pe
   else if (k <= 10) launch_k<D, 10>(ts, Q, perm, nq, k, ids, d2, ctr, st);
   else if (k <= 16) launch_k<D, 16>(ts, Q, perm, nq, k, ids, d2, ctr, st);
   else if (k <= 32) launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else if (k <= kMaxRuntimeK) launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+  else launch_k<D, -1>(ts, Q, perm, nq, k, ids, d2, ctr, st);
 }
 
 template <int D>

@@ -118,6 +118,16 @@ def test_dims_and_k(gk, oracle, d, k):
     run_script(gk, oracle, d, [("insert", P), ("knn", Q, k), ("knn", P[:500], k)], X=256)
 
 
+@pytest.mark.parametrize("d,k", [(2, 257), (3, 600), (7, 300), (3, 5000)])
+def test_large_k_global_heap(gk, oracle, d, k):
+    """k above the shared-memory k-buffers (k > 256): per-lane heaps in a global scratch buffer;
+    k = 5000 > n_live for the second script step exercises the padding rows."""
+    rng = np.random.default_rng(7 * d + k)
+    P = rng.random((4000, d))
+    Q = rng.random((300, d))
+    run_script(gk, oracle, d, [("insert", P), ("knn", Q, k), ("knn", P[:200], k)], X=256)
+
+
 @pytest.mark.parametrize("leaf", [1, 2, 8, 32])
 @pytest.mark.parametrize("heur", [0, 1])
 def test_leaf_and_heuristic(gk, oracle, leaf, heur):
@@ -156,7 +166,7 @@ def test_empty_and_short(gk, oracle):
 def test_errors(gk):
     g = gk.BDLTree(3)
     with pytest.raises(NotImplementedError):
-        g.knn(np.zeros((1, 3)), 257)
+        g.knn(np.zeros((1, 3)), gk.MAX_K + 1)
     with pytest.raises(ValueError):
         g.knn(np.zeros((1, 3)), 0)
     with pytest.raises(ValueError):

@@ -92,11 +92,11 @@ def test_range_device(gk, oracle):
     _same(got, want, "device")
 
 
-@pytest.mark.parametrize("d,k", [(2, 1), (3, 10), (7, 16), (3, 255)])
+@pytest.mark.parametrize("d,k", [(2, 1), (3, 10), (7, 16), (3, 255), (3, 300)])
 def test_knn_graph_parity(gk, oracle, d, k):
     rng = np.random.default_rng(200 + d + k)
     g, o = _pair(gk, oracle, d, X=128, leaf=16)
-    n = 2_000 if k == 255 else 12_000
+    n = 2_000 if k >= 255 else 12_000
     P = rng.random((n, d))
     P[n - 300:] = P[:300]  # duplicates at distance 0 with other ids
     for part in np.array_split(P, 4):
@@ -121,7 +121,7 @@ def test_knn_graph_edges(gk, oracle):
     rows, ids, d2 = g.knn_graph(3)  # one point: all padding
     assert rows.tolist() == [0] and (ids == 0xFFFFFFFF).all() and np.isinf(d2).all()
     with pytest.raises(NotImplementedError):
-        g.knn_graph(256)
+        g.knn_graph(gk.MAX_K)
     with pytest.raises(ValueError):
         g.knn_graph(0)
 
