@@ -20,6 +20,9 @@ int main() {
   }
   auto ball = tree.range(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 2), 1e-4);  // range search
   std::printf("range rows %zu %zu\n", ball[0].size(), ball[1].size());
+  auto ball2 = tree.range(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 2),
+                          std::vector<double>{1e-4, 4e-4});  // one squared radius per query
+  std::printf("per-query range rows %zu %zu\n", ball2[0].size(), ball2[1].size());
   std::vector<std::array<double, 3>> lo{{0.4, 0.4, 0.4}}, hi{{0.45, 0.45, 0.45}};
   std::printf("box rows %zu\n", tree.range_box(lo, hi)[0].size());  // orthogonal range search
   const unsigned long long erased = tree.erase(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 10));

@@ -115,6 +115,24 @@ class BDLTree {
     return out;
   }
 
+  /// Range search (ball) with one squared radius per query: r2[i] applies to S[i].
+  template <class PointSet>
+  std::vector<std::vector<Entry>> range(const PointSet& S, const std::vector<double>& r2) {
+    const std::uint64_t nq = S.size();
+    if (r2.size() != nq) throw std::invalid_argument("range: one squared radius per query expected");
+    std::vector<std::uint64_t> counts(nq), offs(nq + 1);
+    detail::check(gk_bdl_range_radii_count(h_, detail::data_of(S), nq, r2.data(), counts.data()));
+    std::uint64_t total = 0;
+    for (auto c : counts) total += c;
+    std::vector<PointId> ids(total ? total : 1);
+    std::vector<double> d2(total ? total : 1);
+    detail::check(gk_bdl_range_radii(h_, detail::data_of(S), nq, r2.data(), offs.data(), ids.data(), d2.data(), total));
+    std::vector<std::vector<Entry>> out(nq);
+    for (std::uint64_t i = 0; i < nq; ++i)
+      for (std::uint64_t j = offs[i]; j < offs[i + 1]; ++j) out[i].emplace_back(d2[j], ids[j]);
+    return out;
+  }
+
   /// Orthogonal range search: per query box [lo_i, hi_i] the ids of the live points inside, ascending.
   template <class PointSet>
   std::vector<std::vector<PointId>> range_box(const PointSet& lo, const PointSet& hi) {

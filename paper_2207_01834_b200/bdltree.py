@@ -79,6 +79,8 @@ def lib():
         L.gk_bdl_range_count.argtypes = [_P, _P, _u64, C.c_double, _P]
         L.gk_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64]
         L.gk_bdl_range_device.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64, C.POINTER(_u64)]
+        L.gk_bdl_range_radii_count.argtypes = [_P, _P, _u64, _P, _P]
+        L.gk_bdl_range_radii.argtypes = [_P, _P, _u64, _P, _P, _P, _P, _u64]
         L.gk_bdl_range_box_count.argtypes = [_P, _P, _P, _u64, _P]
         L.gk_bdl_range_box.argtypes = [_P, _P, _P, _u64, _P, _P, _u64]
         L.gk_bdl_range_box_device.argtypes = [_P, _P, _P, _u64, _P, _P, _u64, C.POINTER(_u64)]
@@ -137,7 +139,8 @@ class BDLTree:
       insert(P)        Insert_L  (bdl_insert; bdl_build on an empty tree)
       erase(P) -> int  Erase_L   (bdl_erase), returns #points tombstoned
       knn(S, k)        kNN_L     (bdl_knn) -> (ids uint32 (n,k), sqdist float64 (n,k))
-      range(S, r2)     range search (ball) -> (offsets uint64 (n+1,), ids, sqdist) rows sorted by (d2, id)
+      range(S, r2)     range search (ball; r2 scalar or one per query) -> (offsets uint64 (n+1,), ids, sqdist)
+                       rows sorted by (d2, id)
       range_count(S, r2) -> counts uint64 (n,)
       range_box(lo, hi) orthogonal range search -> (offsets uint64 (n+1,), ids ascending)
       knn_graph(k)     k-NN graph -> (row ids (m,), ids (m,k), sqdist (m,k)), one row per live point
@@ -190,20 +193,41 @@ class BDLTree:
         _check(lib().gk_bdl_knn(self._h, _ptr(q), q.shape[0], int(k), _ptr(ids), _ptr(d2)))
         return ids, d2
 
-    def range_count(self, queries, r2: float) -> np.ndarray:
+    @staticmethod
+    def _radii(r2, n):
+        """None for one scalar squared radius, else the per-query radii as a contiguous float64 (n,) array"""
+        if np.ndim(r2) == 0:
+            return None
+        r = np.ascontiguousarray(r2, dtype=np.float64)
+        if r.shape != (n,):
+            raise ValueError(f"per-query r2 must have shape ({n},), got {r.shape}")
+        return r
+
+    def range_count(self, queries, r2) -> np.ndarray:
+        """r2: one squared radius, or one per query (gk_bdl_range_radii_count)"""
         q = _rows(queries, self.d)
         out = np.empty(q.shape[0], np.uint64)
-        _check(lib().gk_bdl_range_count(self._h, _ptr(q), q.shape[0], float(r2), _ptr(out)))
+        rq = self._radii(r2, q.shape[0])
+        if rq is None:
+            _check(lib().gk_bdl_range_count(self._h, _ptr(q), q.shape[0], float(r2), _ptr(out)))
+        else:
+            _check(lib().gk_bdl_range_radii_count(self._h, _ptr(q), q.shape[0], _ptr(rq), _ptr(out)))
         return out
 
-    def range(self, queries, r2: float):
-        """Ball range search: every live point with d2 <= r2, per query sorted by (d2, id)."""
+    def range(self, queries, r2):
+        """Ball range search: every live point with d2 <= r2 (one squared radius, or one per query),
+        per query sorted by (d2, id)."""
         q = _rows(queries, self.d)
         offs = np.zeros(q.shape[0] + 1, np.uint64)
         cap = int(self.range_count(q, r2).sum()) if q.shape[0] else 0
         ids = np.empty(max(cap, 1), np.uint32)
         d2 = np.empty(max(cap, 1), np.float64)
-        _check(lib().gk_bdl_range(self._h, _ptr(q), q.shape[0], float(r2), _ptr(offs), _ptr(ids), _ptr(d2), cap))
+        rq = self._radii(r2, q.shape[0])
+        if rq is None:
+            _check(lib().gk_bdl_range(self._h, _ptr(q), q.shape[0], float(r2), _ptr(offs), _ptr(ids), _ptr(d2), cap))
+        else:
+            _check(lib().gk_bdl_range_radii(self._h, _ptr(q), q.shape[0], _ptr(rq), _ptr(offs), _ptr(ids), _ptr(d2),
+                                            cap))
         return offs, ids[:cap], d2[:cap]
 
     def range_box_count(self, lo, hi) -> np.ndarray:

@@ -891,8 +891,8 @@ constexpr unsigned kRangeSlots = 16;
 constexpr std::uint64_t kRangeSlotBytes = 4ULL << 30;
 static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, double r2,
                                        unsigned long long* counts_dev, unsigned long long* offs_dev, std::uint32_t* ids_dev,
-                                       double* d2_dev, std::uint64_t capacity) {
-  need(!std::isnan(r2) && r2 >= 0.0, "r2 must be a non-negative squared radius");
+                                       double* d2_dev, std::uint64_t capacity, const double* r2q_dev = nullptr) {
+  if (!r2q_dev) need(!std::isnan(r2) && r2 >= 0.0, "r2 must be a non-negative squared radius");
   if (nq >= 0x7fffffffULL) throw Error(GK_ERR_INVALID, "range batch larger than 2^31-1 queries");
   if (nq == 0) {
     if (offs_dev) GK_CUDA(cudaMemsetAsync(offs_dev, 0, 8, h->st));
@@ -922,9 +922,9 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
     if (slots) {
       ti = dalloc<std::uint32_t>(nq * kRangeSlots, h->st);
       td = dalloc<double>(nq * kRangeSlots, h->st);
-      range_launch(h->d, ts, q_dev, nq, r2, perm, cnt, nullptr, ti, td, 2, kRangeSlots, h->st);
+      range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, cnt, nullptr, ti, td, 2, kRangeSlots, h->st);
     } else {
-      range_launch(h->d, ts, q_dev, nq, r2, perm, cnt, nullptr, nullptr, nullptr, 0, 0, h->st);
+      range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, cnt, nullptr, nullptr, nullptr, 0, 0, h->st);
     }
   }
   if (offs_dev) {
@@ -949,10 +949,10 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
           const std::uint64_t no =
               range_slots_compact(nq, kRangeSlots, perm, cnt, offs_dev, ti, td, ids_dev, d2_dev, ovf, h->st);
           if (no)  // the overflowing queries again (in K2 order), rows straight to their offsets
-            range_launch(h->d, ts, q_dev, no, r2, ovf, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
+            range_launch(h->d, ts, q_dev, no, r2, r2q_dev, ovf, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
           dfree(ovf, h->st);
         } else {
-          range_launch(h->d, ts, q_dev, nq, r2, perm, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
+          range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
         }
         range_sort(ids_dev, d2_dev, total, offs_dev, nq, h->st);
       }
@@ -1028,6 +1028,78 @@ int gk_bdl_range_device(gk_bdl* h, const double* q_dev, uint64_t nq, double r2, 
     const std::uint64_t t = range_device_impl(h, q_dev, nq, r2, nullptr, reinterpret_cast<unsigned long long*>(offsets_dev),
                                               ids_dev, d2_dev, capacity);
     if (total) *total = t;
+  });
+}
+
+// Ball range search with one squared radius per query (ParGeo's range search is called per query point with
+// its own radius): the same traversal, each lane's threshold read from r2[query].
+static void check_radii(const double* r2, std::uint64_t nq) {
+  for (std::uint64_t i = 0; i < nq; ++i)
+    need(!std::isnan(r2[i]) && r2[i] >= 0.0, "r2[" + std::to_string(i) + "] must be a non-negative squared radius");
+}
+
+int gk_bdl_range_radii_count(gk_bdl* h, const double* q, uint64_t nq, const double* r2, uint64_t* counts) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(nq == 0 || (q && r2 && counts), "null buffer");
+    check_radii(r2, nq);
+    DevScope ds(h->device);
+    if (nq == 0) return;
+    double* dq = dalloc<double>(nq * h->d, h->st);
+    double* dr = dalloc<double>(nq, h->st);
+    unsigned long long* dc = dalloc<unsigned long long>(nq, h->st);
+    GK_CUDA(cudaMemcpyAsync(dq, q, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    GK_CUDA(cudaMemcpyAsync(dr, r2, nq * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    range_device_impl(h, dq, nq, 0.0, dc, nullptr, nullptr, nullptr, 0, dr);
+    GK_CUDA(cudaMemcpyAsync(counts, dc, nq * 8, cudaMemcpyDeviceToHost, h->st));
+    dfree(dq, h->st);
+    dfree(dr, h->st);
+    dfree(dc, h->st);
+    GK_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int gk_bdl_range_radii(gk_bdl* h, const double* q, uint64_t nq, const double* r2, uint64_t* offsets, uint32_t* ids,
+                       double* d2, uint64_t capacity) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(offsets != nullptr && (nq == 0 || (q && r2)), "null buffer");
+    need(capacity == 0 || (ids && d2), "null row buffers");
+    check_radii(r2, nq);
+    DevScope ds(h->device);
+    if (nq == 0) {
+      offsets[0] = 0;
+      return;
+    }
+    double* dq = dalloc<double>(nq * h->d, h->st);
+    double* dr = dalloc<double>(nq, h->st);
+    unsigned long long* doff = dalloc<unsigned long long>(nq + 1, h->st);
+    std::uint32_t* di = dalloc<std::uint32_t>(std::max<std::uint64_t>(capacity, 1), h->st);
+    double* dd = dalloc<double>(std::max<std::uint64_t>(capacity, 1), h->st);
+    GK_CUDA(cudaMemcpyAsync(dq, q, nq * h->d * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    GK_CUDA(cudaMemcpyAsync(dr, r2, nq * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    auto release = [&] {
+      dfree(dq, h->st);
+      dfree(dr, h->st);
+      dfree(doff, h->st);
+      dfree(di, h->st);
+      dfree(dd, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+    };
+    std::uint64_t total = 0;
+    try {
+      total = range_device_impl(h, dq, nq, 0.0, nullptr, doff, di, dd, capacity, dr);
+    } catch (...) {
+      cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);  // offsets even when the rows do not fit
+      release();
+      throw;
+    }
+    GK_CUDA(cudaMemcpyAsync(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost, h->st));
+    if (total) {
+      GK_CUDA(cudaMemcpyAsync(ids, di, total * 4, cudaMemcpyDeviceToHost, h->st));
+      GK_CUDA(cudaMemcpyAsync(d2, dd, total * 8, cudaMemcpyDeviceToHost, h->st));
+    }
+    release();
   });
 }
 

@@ -182,7 +182,8 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
 // range search (ball, d2 <= r2): K2 order, count / fill passes over the same order, per-query sort
 void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st);
 // mode 0: counts; 1: rows at offs; 2: the first capq rows of query i at ids/d2 + i * capq, and counts
-void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const std::uint32_t* perm,
+void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const double* r2q,
+                  const std::uint32_t* perm,
                   unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, int mode,
                   unsigned capq, cudaStream_t st);
 // slot rows into CSR; returns the number of overflowing queries, listed in K2 order in ovf

@@ -658,6 +658,7 @@ __global__ void k_drop_self(std::uint64_t n, int k, const std::uint32_t* __restr
 template <int D, int MODE>
 __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* __restrict__ Q,
                                                const std::uint32_t* __restrict__ perm, std::uint64_t nq, double r2,
+                                               const double* __restrict__ r2q,
                                                unsigned long long* __restrict__ counts,
                                                const unsigned long long* __restrict__ offs,
                                                std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
@@ -693,8 +694,9 @@ __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* _
       qlo2[j] = pk2(lo, lo);
       qhi2[j] = pk2(hi, hi);
     }
-    const float rf = active ? __double2float_ru(r2) : -1.f;
-    const double rq = active ? r2 : -1.0;
+    const double r2v = (r2q && active) ? r2q[orig] : r2;  // per-query squared radius when given
+    const float rf = active ? __double2float_ru(r2v) : -1.f;
+    const double rq = active ? r2v : -1.0;
     unsigned long long cnt = 0;
     const unsigned long long base =
         (FILL && active) ? offs[orig] : (SLOTS ? static_cast<unsigned long long>(orig) * capq : 0ULL);
@@ -768,7 +770,7 @@ __global__ void __launch_bounds__(256) k_range(const TreeSet ts, const double* _
 }
 
 template <int D>
-void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, unsigned long long* counts,
+void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, const double* r2q, unsigned long long* counts,
              unsigned long long* offs, std::uint32_t* ids, double* d2, int mode, unsigned capq, std::uint32_t* perm,
              cudaStream_t st) {
   static int grid = 0;
@@ -786,9 +788,9 @@ void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, un
   unsigned* tile_ctr = nullptr;
   GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
   GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
-  if (mode == 1) k_range<D, 1><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr, capq);
-  else if (mode == 2) k_range<D, 2><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr, capq);
-  else k_range<D, 0><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, counts, offs, ids, d2, tile_ctr, capq);
+  if (mode == 1) k_range<D, 1><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, r2q, counts, offs, ids, d2, tile_ctr, capq);
+  else if (mode == 2) k_range<D, 2><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, r2q, counts, offs, ids, d2, tile_ctr, capq);
+  else k_range<D, 0><<<g, 256, 0, st>>>(ts, Q, perm, nq, r2, r2q, counts, offs, ids, d2, tile_ctr, capq);
   GK_CHECK_LAUNCH();
   GK_CUDA(cudaFreeAsync(tile_ctr, st));
 }
@@ -1005,14 +1007,15 @@ void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* pe
   }
 }
 
-void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const std::uint32_t* perm,
+void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_t nq, double r2, const double* r2q,
+                  const std::uint32_t* perm,
                   unsigned long long* counts, const unsigned long long* offs, std::uint32_t* ids, double* d2, int mode,
                   unsigned capq, cudaStream_t st) {
   if (nq == 0) return;
   switch (d) {
 #define GK_D(DD)                                                                                                \
   case DD:                                                                                                      \
-    range_d<DD>(trees, q_dev, nq, r2, counts, const_cast<unsigned long long*>(offs), ids, d2, mode, capq,      \
+    range_d<DD>(trees, q_dev, nq, r2, r2q, counts, const_cast<unsigned long long*>(offs), ids, d2, mode, capq,      \
                 const_cast<std::uint32_t*>(perm), st);                                                          \
     break;
     GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)

@@ -49,6 +49,36 @@ def test_range_parity(gk, oracle, d):
     _same(g.range(Q, 0.0), o.range(Q, 0.0), f"d={d} r2=0")
 
 
+@pytest.mark.parametrize("d", [2, 3, 7])
+def test_range_per_query_radii(gk, oracle, d):
+    """one squared radius per query (gk_bdl_range_radii*): each query's rows equal the oracle's
+    single-radius range search of that query with its own radius (0, +inf and duplicates included)"""
+    rng = np.random.default_rng(300 + d)
+    g, o = _pair(gk, oracle, d, X=256, leaf=8)
+    P = rng.random((8_000, d))
+    P[7_000:7_200] = P[:200]
+    for part in np.array_split(P, 3):
+        g.insert(part); o.insert(part)
+    E = P[rng.choice(len(P), 800, replace=False)]
+    assert g.erase(E) == o.erase(E)
+    Q = np.concatenate([rng.random((400, d)), P[:100]])
+    r2 = (rng.random(len(Q)) * 40.0 / len(P)) ** (2.0 / d)
+    r2[::37] = 0.0
+    r2[5] = np.inf
+    parts = [o.range(Q[i:i + 1], float(r2[i])) for i in range(len(Q))]
+    want_counts = np.array([int(p[0][-1]) for p in parts], np.uint64)
+    want = (np.concatenate([[0], np.cumsum(want_counts)]).astype(np.uint64),
+            np.concatenate([p[1] for p in parts]), np.concatenate([p[2] for p in parts]))
+    assert np.array_equal(g.range_count(Q, r2), want_counts)
+    _same(g.range(Q, r2), want, f"d={d} per-query r2")
+    with pytest.raises(ValueError):
+        g.range(Q, np.full(len(Q), -1.0))
+    with pytest.raises(ValueError):
+        g.range_count(Q, np.full(len(Q), np.nan))
+    with pytest.raises(ValueError):
+        g.range(Q, r2[:-1])
+
+
 def test_range_edges(gk, oracle):
     g, o = _pair(gk, oracle, 3)
     Q = np.random.default_rng(1).random((50, 3))
