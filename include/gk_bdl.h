@@ -129,6 +129,8 @@ int gk_bdl_range_device(gk_bdl* h, const double* q_dev, uint64_t nq, double r2, 
 int gk_bdl_range_radii_count(gk_bdl* h, const double* q, uint64_t nq, const double* r2, uint64_t* counts);
 int gk_bdl_range_radii(gk_bdl* h, const double* q, uint64_t nq, const double* r2, uint64_t* offsets, uint32_t* ids,
                        double* d2, uint64_t capacity);
+int gk_bdl_range_radii_device(gk_bdl* h, const double* q_dev, uint64_t nq, const double* r2_dev, uint64_t* offsets_dev,
+                              uint32_t* ids_dev, double* d2_dev, uint64_t capacity, uint64_t* total);
 
 /* Orthogonal (box) range search: for every query box [lo_i, hi_i] (row-major nq x dim each), the
  * ids of the live points p with lo_i[j] <= p[j] <= hi_i[j] for all j, ascending; offsets / capacity

@@ -81,6 +81,7 @@ def lib():
         L.gk_bdl_range_device.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64, C.POINTER(_u64)]
         L.gk_bdl_range_radii_count.argtypes = [_P, _P, _u64, _P, _P]
         L.gk_bdl_range_radii.argtypes = [_P, _P, _u64, _P, _P, _P, _P, _u64]
+        L.gk_bdl_range_radii_device.argtypes = [_P, _P, _u64, _P, _P, _P, _P, _u64, C.POINTER(_u64)]
         L.gk_bdl_range_box_count.argtypes = [_P, _P, _P, _u64, _P]
         L.gk_bdl_range_box.argtypes = [_P, _P, _P, _u64, _P, _P, _u64]
         L.gk_bdl_range_box_device.argtypes = [_P, _P, _P, _u64, _P, _P, _u64, C.POINTER(_u64)]
@@ -274,10 +275,19 @@ class BDLTree:
                                                _ptr(d2_dev), C.byref(c)))
         return c.as_dict()
 
-    def range_device(self, q_dev, r2: float, offs_dev, ids_dev, d2_dev, capacity: int) -> int:
+    def range_device(self, q_dev, r2, offs_dev, ids_dev, d2_dev, capacity: int) -> int:
+        """r2: one squared radius (float) or a device tensor of one per query"""
         t = _u64(0)
-        _check(lib().gk_bdl_range_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), float(r2), _ptr(offs_dev),
-                                         _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
+        if np.ndim(r2) == 0 and not hasattr(r2, "data_ptr"):
+            _check(lib().gk_bdl_range_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), float(r2), _ptr(offs_dev),
+                                             _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
+        else:
+            if tuple(r2.shape) != (int(q_dev.shape[0]),):
+                raise ValueError(f"per-query r2 must have shape ({int(q_dev.shape[0])},), got {tuple(r2.shape)}")
+            if not str(r2.dtype).endswith("float64") or not r2.is_contiguous():
+                raise ValueError("per-query r2 must be a contiguous float64 device tensor")
+            _check(lib().gk_bdl_range_radii_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), _ptr(r2), _ptr(offs_dev),
+                                                   _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
         return int(t.value)
 
     def range_box_device(self, lo_dev, hi_dev, offs_dev, ids_dev, capacity: int) -> int:

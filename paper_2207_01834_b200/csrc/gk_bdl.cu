@@ -69,6 +69,12 @@ __global__ void k_ingest(const double* __restrict__ aos, int d, std::uint64_t n,
   if (ids) ids[i] = static_cast<std::uint32_t>(id_base + i);
 }
 
+// flags a squared radius that is NaN or negative (per-query range search on device pointers)
+__global__ void k_check_radii(const double* __restrict__ r2, std::uint64_t n, int* bad) {
+  std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n && !(r2[i] >= 0.0)) *bad = 1;
+}
+
 // copy SoA rows [0, n) from (src, sstride) to (dst, dstride)
 __global__ void k_copy_soa(const double* __restrict__ src, std::uint64_t sstride, const std::uint32_t* __restrict__ sids,
                            double* __restrict__ dst, std::uint64_t dstride, std::uint32_t* __restrict__ dids, int d,
@@ -1100,6 +1106,28 @@ int gk_bdl_range_radii(gk_bdl* h, const double* q, uint64_t nq, const double* r2
       GK_CUDA(cudaMemcpyAsync(d2, dd, total * 8, cudaMemcpyDeviceToHost, h->st));
     }
     release();
+  });
+}
+
+int gk_bdl_range_radii_device(gk_bdl* h, const double* q_dev, uint64_t nq, const double* r2_dev, uint64_t* offsets_dev,
+                              uint32_t* ids_dev, double* d2_dev, uint64_t capacity, uint64_t* total) {
+  return guard([&] {
+    need(h != nullptr && offsets_dev != nullptr, "null handle/offsets");
+    need(nq == 0 || (q_dev && r2_dev), "null queries/radii");
+    DevScope ds(h->device);
+    if (nq > 0) {
+      int* bad = dalloc<int>(1, h->st);
+      int hb = 0;
+      GK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), h->st));
+      k_check_radii<<<blocks_for(nq), 256, 0, h->st>>>(r2_dev, nq, bad);
+      GK_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      dfree(bad, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+      need(hb == 0, "every r2 must be a non-negative squared radius");
+    }
+    const std::uint64_t t = range_device_impl(h, q_dev, nq, 0.0, nullptr, reinterpret_cast<unsigned long long*>(offsets_dev),
+                                              ids_dev, d2_dev, capacity, r2_dev);
+    if (total) *total = t;
   });
 }
 

@@ -79,6 +79,35 @@ def test_range_per_query_radii(gk, oracle, d):
         g.range(Q, r2[:-1])
 
 
+def test_range_per_query_radii_device(gk, oracle):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(31)
+    g, o = _pair(gk, oracle, 3)
+    P = rng.random((30_000, 3))
+    g.insert(P); o.insert(P)
+    Q = rng.random((2_000, 3))
+    r2 = rng.random(len(Q)) * 2e-3
+    want = g.range(Q, r2)  # host per-query path (checked against the oracle above)
+    ref = [o.range(Q[i:i + 1], float(r2[i])) for i in range(0, len(Q), 97)]
+    for j, i in enumerate(range(0, len(Q), 97)):  # sampled rows straight against the oracle
+        a, b = int(want[0][i]), int(want[0][i + 1])
+        assert np.array_equal(want[1][a:b], ref[j][1]) and np.array_equal(want[2][a:b], ref[j][2])
+    total = int(want[0][-1])
+    qd, rd = torch.from_numpy(Q).cuda(), torch.from_numpy(r2).cuda()
+    offs = torch.zeros(len(Q) + 1, dtype=torch.int64, device="cuda")
+    ids = torch.zeros(total, dtype=torch.int32, device="cuda")
+    d2 = torch.zeros(total, dtype=torch.float64, device="cuda")
+    assert g.range_device(qd, rd, offs, ids, d2, total) == total
+    got = (offs.cpu().numpy().view(np.uint64), ids.cpu().numpy().view(np.uint32), d2.cpu().numpy())
+    _same(got, want, "device per-query r2")
+    rd[7] = -1.0
+    with pytest.raises(ValueError):
+        g.range_device(qd, rd, offs, ids, d2, total)
+    rd[7] = float("nan")
+    with pytest.raises(ValueError):
+        g.range_device(qd, rd, offs, ids, d2, total)
+
+
 def test_range_edges(gk, oracle):
     g, o = _pair(gk, oracle, 3)
     Q = np.random.default_rng(1).random((50, 3))
