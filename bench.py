@@ -328,7 +328,20 @@ def run_gpu(args):
             t0 = time.perf_counter()
             g.range_device(qr, r2, offs, rids, rd2, cap)
             rng_ms.append(1000 * (time.perf_counter() - t0))
-        del rids, rd2, offs
+        del rids, rd2
+        # per-query radii: each query's own k-th neighbour squared distance (>= k rows per query)
+        r2q = d2_dev[:nr, k - 1].contiguous()
+        rq_ms = []
+        for rep in range(3):
+            if rep == 0:
+                capq = g.range_device(qr, r2q, offs, None, None, 0)
+                rids = torch.empty(capq, dtype=torch.int32, device=dev)
+                rd2 = torch.empty(capq, dtype=torch.float64, device=dev)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            g.range_device(qr, r2q, offs, rids, rd2, capq)
+            rq_ms.append(1000 * (time.perf_counter() - t0))
+        del rids, rd2, offs, r2q
         live = g.info()["live"]
         kg = 10
         rows = torch.empty(live, dtype=torch.int32, device=dev)
@@ -347,6 +360,11 @@ def run_gpu(args):
                              "rows": cap, "rows_per_query": cap / nr,
                              "note": "ball range search through gk_bdl_range_device (count pass, scan, fill pass, "
                                      "per-query (d2, id) sort), device-resident queries, best of 2 warm runs"},
+            "range_search_radii": {"queries_per_s": nr / (min(rq_ms[1:]) / 1000.0), "ms": min(rq_ms[1:]),
+                                   "queries": nr, "rows": capq, "rows_per_query": capq / nr,
+                                   "r2_rule": f"each query's own {k}-th neighbour squared distance",
+                                   "note": "gk_bdl_range_radii_device (radii validated on the GPU, count pass, scan, "
+                                           "fill pass, per-query sort), best of 2 warm runs"},
             "knn_graph": {"rows_per_s": live / (min(gr_ms[1:]) / 1000.0), "ms": min(gr_ms[1:]), "rows": live, "k": kg,
                           "note": "gk_bdl_knn_graph_device over every live point (gather + id sort + kNN_L k+1 + "
                                   "self drop), best of 2 warm runs"},
