@@ -113,6 +113,10 @@ def test_range_edges(gk, oracle):
     Q = np.random.default_rng(1).random((50, 3))
     offs, ids, d2 = g.range(Q, 1.0)  # empty structure
     assert not offs.any() and len(ids) == 0
+    offs, ids, d2 = g.range(Q, np.full(len(Q), 1.0))  # empty structure, per-query radii
+    assert not offs.any() and len(ids) == 0
+    offs, ids, d2 = g.range(Q[:0], np.zeros(0))  # no queries, per-query radii
+    assert offs.tolist() == [0] and len(ids) == 0
     P = np.random.default_rng(2).random((3_000, 3))
     g.insert(P); o.insert(P)
     _same(g.range(Q, np.inf), o.range(Q, np.inf), "r2=inf")  # every live point, sorted
