@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the range-search / kNN-graph lines")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C4/C5 lines beside the C2 metric")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time for cpu_baseline")
     return ap.parse_args()
 
@@ -51,6 +52,23 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def load_k1_ncu(cfg: int) -> dict:
+    """profiles/k1_traffic.json (written by profiles/ncu_digest.py --k1-json from an ncu --set full capture
+    of K1 on this workload) when it is for this config, else {}"""
+    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        tj = json.load(open(tp))
+        return tj if tj.get("config") == cfg else {}
+    except (OSError, ValueError):
+        return {}
+
+
+def k1_source_sha() -> str:
+    sys.path.insert(0, os.path.join(ROOT, "profiles"))
+    from ncu_digest import k1_source_sha as f
+    return f()
 
 
 def measured_peaks():
@@ -151,9 +169,11 @@ def cpu_model():
     return "unknown"
 
 
-def config_inputs(cfg: int, scale: float):
+def config_inputs(cfg: int, scale: float, gen=None):
+    """`gen`: the generator module (the reference arm passes the oracle's, so that process never maps
+    libgkbdl.so; the two restatements are bit-identical, tests/test_inputs.py)"""
     from paper_2207_01834_b200.configs import make_inputs
-    d, script = make_inputs(cfg, scale)
+    d, script = make_inputs(cfg, scale, gen=gen)
     P = [op[1] for op in script if op[0] == "insert"]
     K = [op for op in script if op[0] == "knn"]
     return d, P[0], K[0][1], K[0][2]
@@ -190,7 +210,10 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    d, P, Q, k = config_inputs(args.config, args.scale)
+    from oracle import oracle as O
+    if not os.path.exists(O.LIB_PATH):
+        O.build(ref=False)
+    d, P, Q, k = config_inputs(args.config, args.scale, gen=O)
     o, threads, build_s, m = cpu_knn_rate(P, Q, k, d, target_s=max(2.0, args.cpu_seconds / max(1, args.steps)),
                                           sample_cap=len(Q))
     from oracle import oracle as O  # noqa: F401
@@ -306,6 +329,22 @@ def run_gpu(args):
         assert rc == 0, gk.lib().gk_last_error()
     e2e_t = max_over_ranks(sum(e2e_s), device=dev)
     e2e = whole_job_rate(nq * len(e2e_s), world, e2e_t)
+    # the same call from pageable (std::vector-like) host buffers: the reference-side binding's path
+    del Qh, ids_h, d2_h
+    Qp = np.array(Q, copy=True)
+    ids_p = np.empty((nq, k), np.uint32)
+    d2_p = np.empty((nq, k), np.float64)
+    rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, nq, k, ids_p.ctypes.data, d2_p.ctypes.data)  # warm
+    assert rc == 0, gk.lib().gk_last_error()
+    pg_s = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, nq, k, ids_p.ctypes.data, d2_p.ctypes.data)
+        pg_s.append(time.perf_counter() - t0)
+        assert rc == 0, gk.lib().gk_last_error()
+    e2e_pageable = whole_job_rate(nq * len(pg_s), world, max_over_ranks(sum(pg_s), device=dev))
+    del Qp, ids_p, d2_p
 
     # ---- §8f-4 consumers of the same structure (reported beside the metric, not part of it):
     # ball range search (count + fill + per-query sort) and the k-NN graph over every live point
@@ -370,21 +409,49 @@ def run_gpu(args):
                                   "self drop), best of 2 warm runs"},
         }
 
+    # ---- the other BASELINE configs beside the metric (C1, C3, C4, C5; not part of `value`)
+    configs = None
+    if not args.no_configs and args.config == 2 and args.scale == 1.0:
+        configs = {}
+        for c in (1, 3, 4, 5):
+            configs[f"C{c}"] = config_line(c, dev)
+
     if rank == 0:
         hbm, peak_src = measured_peaks()
         fp64_peak = measure_fp64_peak(dev)
         k1_ms = statistics.mean(trav_ms)
         achieved = bytes_per_q * nq / (k1_ms / 1000.0) / 1e9
-        traffic = issue_pct = None
-        tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
-        if os.path.exists(tp):
-            try:
-                tj = json.load(open(tp))
-                if tj.get("config") == args.config:
-                    traffic = tj.get("dram_bytes_per_launch")
-                    issue_pct = tj.get("issue_active_pct")
-            except Exception:
-                traffic = None
+        ncu = load_k1_ncu(args.config)
+        traffic = ncu.get("dram_bytes_per_launch")
+        clk_sum = clk.summary()
+        sm_mhz = clk_sum.get("sm_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        l2_peak = gk.l2_read_gbs(dev.index)
+        # warp-requested bytes: what the warps actually load (one node record per warp node visit,
+        # one staged point (8D + 4 B) per point of every warp leaf visit)
+        warp_bytes = ctr["warp_nodes"] * 16 * (d + 1) + ctr["warp_leaf_points"] * (8 * d + 4)
+        ceilings = {
+            "l2": {"achieved": warp_bytes / (k1_ms / 1000.0) / 1e9, "peak": l2_peak, "unit": "GB/s",
+                   "frac": warp_bytes / (k1_ms / 1000.0) / 1e9 / l2_peak, "bytes_per_launch": warp_bytes,
+                   "definition": "warp-requested bytes (warp node visits x sizeof(TNode<D>) + warp-leaf points x "
+                                 "(8D + 4), counted by the instrumented pass) / live K1 time / L2 read bandwidth "
+                                 "measured live on this GPU (gk_diag_l2_read_gbs: 16-byte ld.global.cg over an "
+                                 "L2-resident 32 MiB buffer)"},
+        }
+        if ncu.get("warp_instructions"):
+            insts = float(ncu["warp_instructions"])
+            cap = 4 * sms * sm_mhz * 1e6 * (k1_ms / 1000.0)  # one warp instruction per SMSP per cycle
+            ceilings["issue"] = {"achieved": insts / (k1_ms / 1000.0) / 1e9, "peak": 4 * sms * sm_mhz / 1e3,
+                                 "unit": "G warp-inst/s", "frac": insts / cap, "insts_per_query": insts / nq,
+                                 "ncu_issue_active_pct": ncu.get("issue_active_pct"),
+                                 "stale": ncu.get("k1_source_sha") != k1_source_sha(),
+                                 "definition": "K1 warp instructions (ncu smsp__inst_executed.sum of the same "
+                                               "workload, profiles/k1_traffic.json) / (4 SMSPs x SMs x sampled "
+                                               "SM clock x live K1 time)"}
+        if traffic:
+            ceilings["dram"] = {"achieved": traffic / (k1_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                                "frac": traffic / (k1_ms / 1000.0) / 1e9 / hbm,
+                                "definition": "ncu dram__bytes_read + dram__bytes_write of K1 / live K1 time"}
         cpu = None
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is reported at N=1 only
             o, threads, build_s, m = cpu_knn_rate(P, Q, k, d, args.cpu_seconds, sample_cap=len(Q))
@@ -401,22 +468,32 @@ def run_gpu(args):
             "config": workload_desc(args.config, len(P), nq, k, d),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_source": peak_src,
+                         "frac_definition": "north-star (BASELINE.json) traversal roofline, kept as the legacy "
+                                            "figure: bytes of the nodes and leaf points each query itself needed "
+                                            "(instrumented pass) at HBM peak.  L1/L2 hits are charged at the HBM "
+                                            "rate, so it is not a ceiling (> 1 possible); the ceilings below are",
                          "kernel": "k_knn (K1 fused kNN_L traversal)", "k1_ms": k1_ms,
                          "bytes_per_query": bytes_per_q, "flops_per_query": flops_per_q,
                          "fp64_gflops": flops_per_q * nq / (k1_ms / 1000.0) / 1e9,
                          "fp64_peak_tflops": fp64_peak,
                          "fp64_frac": flops_per_q * nq / (k1_ms / 1000.0) / 1e12 / fp64_peak if fp64_peak else None,
                          "fp64_peak_source": "measured here: cuBLAS DGEMM 8192^3 via torch, best of 3",
-                         "counters": ctr,
-                         "issue_active_pct": issue_pct,
-                         "issue_note": "ncu smsp__issue_active of this kernel (profiles/k1_traffic.json): the "
-                                       "tree is L1/L2-resident, so K1 is bound by instruction issue, not DRAM"},
+                         "ceilings": ceilings,
+                         "issue_frac": (ceilings.get("issue") or {}).get("frac"),
+                         "l2_frac": ceilings["l2"]["frac"],
+                         "insts_per_query": (ceilings.get("issue") or {}).get("insts_per_query"),
+                         "counters": ctr},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": nq * d * 8,
-                    "d2h_bytes_per_step": nq * k * (4 + 8)},
+                    "d2h_bytes_per_step": nq * k * (4 + 8),
+                    "host_buffers": "pinned (cudaHostAlloc'd by torch.pin_memory)",
+                    "pageable": {"value": e2e_pageable, "unit": "queries/s",
+                                 "note": "the same gk_bdl_knn call from pageable numpy buffers (what a std::vector "
+                                         "caller of geokit_bdl.hpp gets): staged through the handle's pinned ring"}},
             "gpu_launches": 10 * args.steps,  # k_qbox_init, k_qbox, k_curve_key, 6 CUB radix-sort kernels, k_knn
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
             "consumers": extras,
+            "configs": configs,
             "build": {"insert_l_points_per_s": len(P) / build_wall, "buildveb_points_per_s": built / (build_ms / 1000.0),
                       "hbm_frac": build_bytes / (build_ms / 1000.0) / 1e9 / hbm,
                       "algorithmic_bytes": build_bytes,
@@ -433,21 +510,24 @@ def run_gpu(args):
         torch.distributed.destroy_process_group()
 
 
-def run_script(args):
-    """Configs 4/5 (dynamic scripts): replay the whole Insert_L / Erase_L / kNN_L script
-    on the device (inputs pre-staged in HBM); value = kNN_L queries/s over all kNN ops."""
+def replay_script(cfg: int, scale: float, dev, reps: int = 3):
+    """Replays a dynamic config (C4 / C5: Insert_L, Erase_L, kNN_L ops) on `dev` with every op's input
+    pre-staged in HBM; rep 0 warms the memory pool, per op type the best of the later reps.
+    Returns {op: [units, seconds]} with kNN_L also split by k ("knn_k1", "knn_k16", ...)."""
     import torch
     import paper_2207_01834_b200 as gk
-    from paper_2207_01834_b200.configs import CONFIGS, make_inputs
-    rank, world, _ = dist_env()
-    dev = torch.device("cuda", 0)
-    d, script = make_inputs(args.config, args.scale)
+    from paper_2207_01834_b200.configs import make_inputs
+    d, script = make_inputs(cfg, scale)
     staged = [(op[0], torch.from_numpy(op[1]).to(dev)) + tuple(op[2:]) for op in script]
     res = None
-    for rep in range(3):  # rep 0 warms the memory pool; best of reps 1-2 per op type
-        g = gk.BDLTree(d)
-        t = {"insert": [0, 0.0], "erase": [0, 0.0], "knn": [0, 0.0]}
+    for rep in range(reps):
+        g = gk.BDLTree(d, device=dev.index)
+        t = {}
         for op in staged:
+            keys = [op[0]] + ([f"knn_k{op[2]}"] if op[0] == "knn" else [])
+            if op[0] == "knn":
+                ids = torch.empty((op[1].shape[0], op[2]), dtype=torch.int32, device=dev)
+                d2 = torch.empty((op[1].shape[0], op[2]), dtype=torch.float64, device=dev)
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             if op[0] == "insert":
@@ -455,28 +535,95 @@ def run_script(args):
             elif op[0] == "erase":
                 g.erase_device(op[1])
             else:
-                k = op[2]
-                ids = torch.empty((op[1].shape[0], k), dtype=torch.int32, device=dev)
-                d2 = torch.empty((op[1].shape[0], k), dtype=torch.float64, device=dev)
-                torch.cuda.synchronize(dev)
-                t0 = time.perf_counter()
-                g.knn_device(op[1], k, ids, d2)
+                g.knn_device(op[1], op[2], ids, d2)
             torch.cuda.synchronize(dev)
-            t[op[0]][0] += op[1].shape[0]
-            t[op[0]][1] += time.perf_counter() - t0
+            dt = time.perf_counter() - t0
+            for kk in keys:
+                v = t.setdefault(kk, [0, 0.0])
+                v[0] += op[1].shape[0]
+                v[1] += dt
         if rep == 1:
             res = t
         elif rep > 1:
             res = {kk: [v[0], min(v[1], t[kk][1])] for kk, v in res.items()}
         g.close()
+    del staged
+    return res
+
+
+def config_line(cfg: int, dev, steps: int = 3) -> dict:
+    """One BASELINE config measured on `dev` beside the metric (driver-visible): C1 / C3 kNN_L queries/s
+    (device-resident, L2 flushed between steps) and Insert_L points/s; C4 / C5 replayed scripts."""
+    import torch
+    import paper_2207_01834_b200 as gk
+    from paper_2207_01834_b200.configs import CONFIGS
+    if cfg in (4, 5):
+        r = replay_script(cfg, 1.0, dev)
+        out = {"workload": CONFIGS[cfg]["name"],
+               "knn_queries_per_s": r["knn"][0] / r["knn"][1],
+               "insert_l_points_per_s": r["insert"][0] / r["insert"][1],
+               "note": "whole script replayed with every op's input in HBM; per op type the best of 2 warm "
+                       "replays (a first replay warms the memory pool)"}
+        if "erase" in r:
+            out["erase_l_points_per_s"] = r["erase"][0] / r["erase"][1]
+        for kk, v in r.items():
+            if kk.startswith("knn_k"):
+                out[f"{kk}_queries_per_s"] = v[0] / v[1]
+        out["ops_seconds"] = {kk: v[1] for kk, v in r.items()}
+        return out
+    d, P, Q, k = config_inputs(cfg, 1.0)
+    P_dev = torch.from_numpy(P).to(dev)
+    ins = []
+    for rep in range(3):
+        g = gk.BDLTree(d, device=dev.index)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        g.insert_device(P_dev)
+        ins.append(time.perf_counter() - t0)
+        if rep < 2:
+            g.close()
+    del P_dev
+    Q_dev = torch.from_numpy(Q).to(dev)
+    ids = torch.empty((len(Q), k), dtype=torch.int32, device=dev)
+    d2 = torch.empty((len(Q), k), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.ExternalStream(g.stream(), device=dev)
+    g.knn_device(Q_dev, k, ids, d2)
+    ms = []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.knn_device(Q_dev, k, ids, d2)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    g.close()
+    return {"workload": workload_desc(cfg, len(P), len(Q), k, d)["workload"],
+            "knn_queries_per_s": len(Q) * steps / (sum(ms) / 1000.0), "knn_ms": sum(ms) / steps,
+            "insert_l_points_per_s": len(P) / min(ins[1:]),
+            "note": f"kNN_L over the config's {len(Q)} queries, device-resident, mean of {steps} steps with L2 flushed "
+                    f"between them; Insert_L of all {len(P)} points into a fresh handle, best of 2 warm runs"}
+
+
+def run_script(args):
+    """Configs 4/5 (dynamic scripts) as the main line: value = kNN_L queries/s over all kNN ops."""
+    import torch
+    from paper_2207_01834_b200.configs import CONFIGS
+    rank, world, local = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    res = replay_script(args.config, args.scale, dev)
     line = {"metric": "kNN_L queries/s", "value": res["knn"][0] / res["knn"][1], "unit": "queries/s", "n_gpus": 1,
-            "steps": 1, "warmup": 1, "ms_per_step": 1000 * sum(v[1] for v in res.values()), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": 1, "warmup": 1, "ms_per_step": 1000 * sum(v[1] for kk, v in res.items() if "_k" not in kk),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIGS[args.config]["name"], "scale": args.scale},
-            "insert_l_points_per_s": res["insert"][0] / res["insert"][1] if res["insert"][1] else None,
-            "erase_l_points_per_s": res["erase"][0] / res["erase"][1] if res["erase"][1] else None,
+            "insert_l_points_per_s": res["insert"][0] / res["insert"][1] if "insert" in res else None,
+            "erase_l_points_per_s": res["erase"][0] / res["erase"][1] if "erase" in res else None,
             "ops_seconds": {k: v[1] for k, v in res.items()}}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def main():

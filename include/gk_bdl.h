@@ -89,6 +89,8 @@ typedef struct gk_knn_counters {
   uint64_t warp_nodes;   /* node loads actually issued (one per warp tile) */
   uint64_t warp_leaves;  /* leaf loads actually issued (one per warp tile) */
   uint64_t inserts;      /* points accepted into a k-buffer (all queries) */
+  uint64_t warp_leaf_points; /* points of the leaves actually loaded (summed over warp leaf loads) */
+  uint64_t warp_inserts;     /* warp-level k-buffer update events (a warp executing an insert) */
 } gk_knn_counters;
 
 const char* gk_last_error(void);
@@ -108,6 +110,11 @@ int gk_bdl_erase_device(gk_bdl* h, const double* pts_dev, uint64_t n, uint64_t* 
 /* kNN_L: exact k nearest live points of every query, 1 <= k <= GK_MAX_K. */
 int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, double* d2);
 int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev);
+/* Radius-bounded kNN_L: the k nearest live points with d2 <= r2_dev[i] (r2 >= 0, +inf allowed) of
+ * every query, rows as gk_bdl_knn; slots beyond the points within the radius are (GK_NO_POINT, +inf).
+ * With r2 = +inf this is gk_bdl_knn. */
+int gk_bdl_knn_bounded_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, const double* r2_dev,
+                              uint32_t* ids_dev, double* d2_dev);
 /* Instrumented kNN_L (same results) that also counts the work of §8(d). */
 int gk_bdl_knn_counted_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32_t* ids_dev, double* d2_dev,
                               gk_knn_counters* counters);
@@ -164,6 +171,10 @@ int gk_bdl_sync(gk_bdl* h);
 int gk_bdl_last_knn_ms(gk_bdl* h, float* traversal_ms, float* total_ms);
 /* Device time (ms) of the last insert's BuildvEB_S work and #points built. */
 int gk_bdl_last_build_ms(gk_bdl* h, float* build_ms, uint64_t* points_built);
+
+/* Diagnostics: L2 read bandwidth (GB/s) of `device`, streaming 16-byte L2-only loads over an
+ * L2-resident buffer of `bytes` (the ceiling bench.py reports warp-requested bytes against). */
+int gk_diag_l2_read_gbs(int device, uint64_t bytes, double* gbs);
 
 /* Seeded input generators (host, OpenMP), restating geokit/generators.hpp:56-63
  * with side 1 and the BASELINE.json config recipes. */

@@ -46,7 +46,8 @@ class _Info(C.Structure):
 class KnnCounters(C.Structure):
     _fields_ = [("node_bytes", C.c_uint64), ("leaf_bytes", C.c_uint64), ("nodes", C.c_uint64),
                 ("leaves", C.c_uint64), ("dists", C.c_uint64), ("warp_nodes", C.c_uint64),
-                ("warp_leaves", C.c_uint64), ("inserts", C.c_uint64)]
+                ("warp_leaves", C.c_uint64), ("inserts", C.c_uint64), ("warp_leaf_points", C.c_uint64),
+                ("warp_inserts", C.c_uint64)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
@@ -75,6 +76,7 @@ def lib():
         L.gk_bdl_erase_device.argtypes = [_P, _P, _u64, C.POINTER(_u64)]
         L.gk_bdl_knn.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
         L.gk_bdl_knn_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
+        L.gk_bdl_knn_bounded_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, _P]
         L.gk_bdl_knn_counted_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, C.POINTER(KnnCounters)]
         L.gk_bdl_range_count.argtypes = [_P, _P, _u64, C.c_double, _P]
         L.gk_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64]
@@ -95,6 +97,7 @@ def lib():
         L.gk_bdl_sync.argtypes = [_P]
         L.gk_bdl_last_knn_ms.argtypes = [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]
         L.gk_bdl_last_build_ms.argtypes = [_P, C.POINTER(C.c_float), C.POINTER(_u64)]
+        L.gk_diag_l2_read_gbs.argtypes = [C.c_int, _u64, C.POINTER(C.c_double)]
         L.gk_gen_uniform.argtypes = [_u64, C.c_int, _u64, _P]
         L.gk_gen_mixture.argtypes = [_u64, C.c_int, _u64, C.c_int, C.c_double, _P]
         L.gk_gen_walk.argtypes = [_u64, _u64, _u64, _P]
@@ -153,9 +156,33 @@ class BDLTree:
         self.d = int(dim)
         self.X = int(X)
         self.leaf_size = int(leaf_size)
+        self.device = int(device)
         h = _P()
-        _check(lib().gk_bdl_create(self.d, self.X, self.leaf_size, int(heuristic), int(device), C.byref(h)))
+        _check(lib().gk_bdl_create(self.d, self.X, self.leaf_size, int(heuristic), self.device, C.byref(h)))
         self._h = h
+
+    def _dev(self, t, dtype: str, shape: tuple, name: str, optional: bool = False):
+        """Checks a device-API tensor before its raw pointer crosses the C ABI: a CUDA tensor on this
+        handle's device, contiguous, of `dtype`, with `shape` (None entries match any size).  A CPU
+        tensor, a wrong dtype or a strided view would otherwise be read or written as raw memory."""
+        if t is None:
+            if optional:
+                return None
+            raise ValueError(f"{name}: a CUDA tensor is required")
+        if not hasattr(t, "data_ptr") or not getattr(t, "is_cuda", False):
+            raise ValueError(f"{name}: expected a CUDA torch tensor, got {type(t).__name__}"
+                             f"{'' if not hasattr(t, 'device') else ' on ' + str(t.device)}")
+        if t.device.index != self.device:
+            raise ValueError(f"{name}: tensor is on {t.device}, the handle is on cuda:{self.device}")
+        if not str(t.dtype).endswith(dtype):
+            raise ValueError(f"{name}: expected dtype {dtype}, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: tensor must be contiguous")
+        ts = tuple(int(x) for x in t.shape)
+        if len(ts) != len(shape) or any(w is not None and w != g for w, g in zip(shape, ts)):
+            want = "(" + ", ".join("n" if w is None else str(w) for w in shape) + ")"
+            raise ValueError(f"{name}: expected shape {want}, got {ts}")
+        return t
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -258,18 +285,35 @@ class BDLTree:
 
     # ------------------------------------------------------------- device API
     def insert_device(self, pts_dev) -> None:
+        self._dev(pts_dev, "float64", (None, self.d), "pts_dev")
         _check(lib().gk_bdl_insert_device(self._h, _ptr(pts_dev), int(pts_dev.shape[0])))
 
     def erase_device(self, pts_dev) -> int:
+        self._dev(pts_dev, "float64", (None, self.d), "pts_dev")
         n = _u64(0)
         _check(lib().gk_bdl_erase_device(self._h, _ptr(pts_dev), int(pts_dev.shape[0]), C.byref(n)))
         return int(n.value)
 
+    def _knn_args(self, q_dev, k, ids_dev, d2_dev):
+        self._dev(q_dev, "float64", (None, self.d), "q_dev")
+        nq = int(q_dev.shape[0])
+        self._dev(ids_dev, "int32", (nq, int(k)), "ids_dev")
+        self._dev(d2_dev, "float64", (nq, int(k)), "d2_dev")
+
     def knn_device(self, q_dev, k: int, ids_dev, d2_dev) -> None:
+        self._knn_args(q_dev, k, ids_dev, d2_dev)
         _check(lib().gk_bdl_knn_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), int(k), _ptr(ids_dev),
                                        _ptr(d2_dev)))
 
+    def knn_bounded_device(self, q_dev, k: int, r2_dev, ids_dev, d2_dev) -> None:
+        """k nearest within squared radius r2_dev[i] (inclusive); unfilled slots are (NO_POINT, +inf)"""
+        self._knn_args(q_dev, k, ids_dev, d2_dev)
+        self._dev(r2_dev, "float64", (int(q_dev.shape[0]),), "r2_dev")
+        _check(lib().gk_bdl_knn_bounded_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), int(k), _ptr(r2_dev),
+                                               _ptr(ids_dev), _ptr(d2_dev)))
+
     def knn_counted_device(self, q_dev, k: int, ids_dev, d2_dev) -> dict:
+        self._knn_args(q_dev, k, ids_dev, d2_dev)
         c = KnnCounters()
         _check(lib().gk_bdl_knn_counted_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), int(k), _ptr(ids_dev),
                                                _ptr(d2_dev), C.byref(c)))
@@ -277,26 +321,41 @@ class BDLTree:
 
     def range_device(self, q_dev, r2, offs_dev, ids_dev, d2_dev, capacity: int) -> int:
         """r2: one squared radius (float) or a device tensor of one per query"""
+        self._dev(q_dev, "float64", (None, self.d), "q_dev")
+        nq = int(q_dev.shape[0])
+        self._dev(offs_dev, "int64", (nq + 1,), "offs_dev")
+        self._dev(ids_dev, "int32", (None,), "ids_dev", optional=capacity == 0)
+        self._dev(d2_dev, "float64", (None,), "d2_dev", optional=capacity == 0)
+        if ids_dev is not None and (ids_dev.shape[0] < capacity or d2_dev is None or d2_dev.shape[0] < capacity):
+            raise ValueError(f"ids_dev / d2_dev must hold capacity={capacity} rows")
         t = _u64(0)
         if np.ndim(r2) == 0 and not hasattr(r2, "data_ptr"):
             _check(lib().gk_bdl_range_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), float(r2), _ptr(offs_dev),
                                              _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
         else:
-            if tuple(r2.shape) != (int(q_dev.shape[0]),):
-                raise ValueError(f"per-query r2 must have shape ({int(q_dev.shape[0])},), got {tuple(r2.shape)}")
-            if not str(r2.dtype).endswith("float64") or not r2.is_contiguous():
-                raise ValueError("per-query r2 must be a contiguous float64 device tensor")
+            self._dev(r2, "float64", (nq,), "per-query r2")
             _check(lib().gk_bdl_range_radii_device(self._h, _ptr(q_dev), int(q_dev.shape[0]), _ptr(r2), _ptr(offs_dev),
                                                    _ptr(ids_dev), _ptr(d2_dev), int(capacity), C.byref(t)))
         return int(t.value)
 
     def range_box_device(self, lo_dev, hi_dev, offs_dev, ids_dev, capacity: int) -> int:
+        self._dev(lo_dev, "float64", (None, self.d), "lo_dev")
+        nq = int(lo_dev.shape[0])
+        self._dev(hi_dev, "float64", (nq, self.d), "hi_dev")
+        self._dev(offs_dev, "int64", (nq + 1,), "offs_dev")
+        self._dev(ids_dev, "int32", (None,), "ids_dev", optional=capacity == 0)
+        if ids_dev is not None and ids_dev.shape[0] < capacity:
+            raise ValueError(f"ids_dev must hold capacity={capacity} rows")
         t = _u64(0)
         _check(lib().gk_bdl_range_box_device(self._h, _ptr(lo_dev), _ptr(hi_dev), int(lo_dev.shape[0]), _ptr(offs_dev),
                                              _ptr(ids_dev), int(capacity), C.byref(t)))
         return int(t.value)
 
     def knn_graph_device(self, k: int, rows_dev, ids_dev, d2_dev) -> None:
+        n = self.info()["live"]
+        self._dev(rows_dev, "int32", (n,), "rows_dev")
+        self._dev(ids_dev, "int32", (n, int(k)), "ids_dev")
+        self._dev(d2_dev, "float64", (n, int(k)), "d2_dev")
         _check(lib().gk_bdl_knn_graph_device(self._h, int(k), _ptr(rows_dev), _ptr(ids_dev), _ptr(d2_dev)))
 
     # ------------------------------------------------------------ inspection
@@ -342,6 +401,13 @@ class BDLTree:
         a, n = C.c_float(), _u64()
         _check(lib().gk_bdl_last_build_ms(self._h, C.byref(a), C.byref(n)))
         return float(a.value), int(n.value)
+
+
+def l2_read_gbs(device: int = 0, nbytes: int = 32 << 20) -> float:
+    """measured L2 read bandwidth (GB/s) over an L2-resident buffer (gk_diag_l2_read_gbs)"""
+    v = C.c_double()
+    _check(lib().gk_diag_l2_read_gbs(int(device), int(nbytes), C.byref(v)))
+    return float(v.value)
 
 
 # ---------------------------------------------------------------- inputs ---

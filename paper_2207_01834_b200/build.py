@@ -20,7 +20,7 @@ CLI = os.path.join(OUT_DIR, "gk_bdl_cli")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 CU_SOURCES = ["gk_build.cu", "gk_knn.cu", "gk_bdl.cu"]
-CPP_SOURCES = ["gk_gen.cpp"]
+CPP_SOURCES = ["gk_gen.cpp", "gk_host.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -32,6 +32,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "gk_common.cuh"
+#include "gk_host.h"
 
 using namespace gk;
 
@@ -101,13 +102,19 @@ __global__ void k_compact(const double* __restrict__ src, std::uint64_t sstride,
   dids[o] = sids[i];
 }
 
-__global__ void k_gather_ids(std::uint32_t* tree_ids, std::uint32_t* src_idx, const std::uint32_t* __restrict__ arr_ids,
-                             std::uint64_t n) {
+// src[i] = arrival index of tree id ids[i]: binary search in the (id, arrival) pairs sorted by id
+__global__ void k_map_src(const std::uint32_t* __restrict__ ids, std::uint64_t n, const std::uint32_t* __restrict__ skeys,
+                          const std::uint32_t* __restrict__ svals, std::uint32_t* __restrict__ src) {
   std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
-  const std::uint32_t a = tree_ids[i];
-  src_idx[i] = a;
-  tree_ids[i] = arr_ids[a];
+  const std::uint32_t x = ids[i];
+  std::uint64_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const std::uint64_t mid = (lo + hi) / 2;
+    if (skeys[mid] <= x) lo = mid;
+    else hi = mid;
+  }
+  src[i] = svals[lo];
 }
 
 __global__ void k_iota(std::uint32_t* out, std::uint64_t n) {
@@ -203,6 +210,19 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
   }
 }
 
+// L2 read bandwidth probe (the ceiling for traffic that hits in L2): every thread streams
+// 16-byte L2-only loads (ld.global.cg, L1 bypassed) over a buffer that fits in L2
+__global__ void k_l2_read(const ulonglong2* __restrict__ a, std::uint64_t n, int reps, unsigned long long* sink) {
+  unsigned long long acc = 0;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (int r = 0; r < reps; ++r)
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+      const ulonglong2 v = __ldcg(a + i);
+      acc ^= v.x ^ (v.y + static_cast<unsigned long long>(r));
+    }
+  if (acc == 0x9e3779b97f4a7c15ULL) *sink = acc;  // keeps the loads alive
+}
+
 }  // namespace
 
 // GK_TRACE=1: host-side phase timestamps of Insert_L on stderr (diagnostics only)
@@ -247,8 +267,21 @@ struct gk_bdl {
   BuildScratch bscratch[kBuildSlots];
   cudaStream_t bst[kBuildSlots] = {};
   cudaEvent_t ev_pool = nullptr;
+  // pinned staging ring of the pageable-host kNN_L pipeline (allocated on first use)
+  static constexpr int kStageSlots = 4;
+  static constexpr std::size_t kStageBytes = 16u << 20;
+  void* stage[kStageSlots] = {};
+  cudaEvent_t stage_ev[kStageSlots] = {};
 
   std::uint64_t bstride() const { return 2ULL * X; }
+
+  void ensure_stage() {
+    if (stage[0]) return;
+    for (int i = 0; i < kStageSlots; ++i) {
+      GK_CUDA(cudaMallocHost(&stage[i], kStageBytes));
+      GK_CUDA(cudaEventCreateWithFlags(&stage_ev[i], cudaEventDisableTiming));
+    }
+  }
 
   void scan(const std::uint32_t* in, std::uint32_t* out, std::uint64_t n) {
     std::size_t need = 0;
@@ -281,18 +314,28 @@ struct gk_bdl {
     free_tree(buf_tree, st);
     dfree(buf_src, st);
     if (buf_n == 0) return;
-    // build over arrival indices, then map them to ids (keeping the map for erase)
-    std::uint32_t* iota = dalloc<std::uint32_t>(buf_n, st);
-    k_iota<<<blocks_for(buf_n), 256, 0, st>>>(iota, buf_n);
-    tr("  buffer: freed + iota");
-    build_begin(scratch, d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), iota, buf_n, buf_tree, st);
+    // Build_S over the buffer with its real ids (object-median ties break by id, as in every static
+    // tree), then buf_src[pos] = arrival index of the point at tree position pos, for erase compaction:
+    // ids are unique, so sort (id, arrival) and binary-search each tree id.
+    build_begin(scratch, d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), buf_ids, buf_n, buf_tree, st);
     tr("  buffer: k_build done");
     build_finish(scratch);
     tr("  buffer: emitted");
+    std::uint32_t* iota = dalloc<std::uint32_t>(buf_n, st);
+    std::uint32_t* skeys = dalloc<std::uint32_t>(buf_n, st);
+    std::uint32_t* svals = dalloc<std::uint32_t>(buf_n, st);
+    k_iota<<<blocks_for(buf_n), 256, 0, st>>>(iota, buf_n);
+    std::size_t tb = 0;
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, buf_ids, skeys, iota, svals, static_cast<int>(buf_n), 0, 32, st));
+    void* tmp = dalloc<char>(tb, st);
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, buf_ids, skeys, iota, svals, static_cast<int>(buf_n), 0, 32, st));
     buf_src = dalloc<std::uint32_t>(buf_n, st);
-    k_gather_ids<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_src, buf_ids, buf_n);
+    k_map_src<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_n, skeys, svals, buf_src);
     GK_CHECK_LAUNCH();
+    dfree(tmp, st);
     dfree(iota, st);
+    dfree(skeys, st);
+    dfree(svals, st);
   }
 
   // Insert_L of device SoA points (stride sp) with their ids.
@@ -638,6 +681,11 @@ int gk_bdl_destroy(gk_bdl* h) {
     for (auto& e : h->pev) cudaEventDestroy(e);
     for (auto& bs : h->bst) cudaStreamDestroy(bs);
     cudaEventDestroy(h->ev_pool);
+    for (int i = 0; i < gk_bdl::kStageSlots; ++i)
+      if (h->stage[i]) {
+        cudaFreeHost(h->stage[i]);
+        cudaEventDestroy(h->stage_ev[i]);
+      }
     cudaStreamDestroy(h->st);
     delete h;
   });
@@ -720,7 +768,7 @@ int gk_bdl_erase(gk_bdl* h, const double* pts, uint64_t n, uint64_t* n_erased) {
 }
 
 static void knn_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, int k, std::uint32_t* ids_dev,
-                            double* d2_dev, gk_knn_counters* ctr) {
+                            double* d2_dev, gk_knn_counters* ctr, const double* bound = nullptr) {
   need(k >= 1, "k must be >= 1");
   if (k > GK_MAX_K) throw Error(GK_ERR_UNSUPPORTED, "k > " + std::to_string(GK_MAX_K) + " is not supported");
   if (nq == 0) return;
@@ -734,12 +782,12 @@ static void knn_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, in
     GK_CUDA(cudaStreamSynchronize(h->st));
     return;
   }
-  knn_launch(h->d, k, ts, q_dev, nq, ids_dev, d2_dev, ctr, h->st, h->ev[2], h->ev[3]);
+  knn_launch(h->d, k, ts, q_dev, nq, ids_dev, d2_dev, ctr, h->st, h->ev[2], h->ev[3], bound);
   GK_CUDA(cudaEventRecord(h->ev[1], h->st));
   GK_CUDA(cudaStreamSynchronize(h->st));
   GK_CUDA(cudaEventElapsedTime(&h->knn_ms, h->ev[2], h->ev[3]));
   GK_CUDA(cudaEventElapsedTime(&h->knn_total_ms, h->ev[0], h->ev[1]));
-  if (nq >= (1u << 16) && !ctr) {
+  if (nq >= (1u << 16) && !ctr && !bound) {
     h->knn_ns_q = 1e6 * h->knn_total_ms / static_cast<double>(nq);
     h->knn_ns_k = k;
   }
@@ -751,6 +799,66 @@ int gk_bdl_knn_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, uint32
     need(nq == 0 || (q_dev && ids_dev && d2_dev), "null buffer");
     DevScope ds(h->device);
     knn_device_impl(h, q_dev, nq, k, ids_dev, d2_dev, nullptr);
+  });
+}
+
+int gk_diag_l2_read_gbs(int device, uint64_t bytes, double* gbs) {
+  return guard([&] {
+    need(gbs != nullptr, "null output");
+    need(bytes >= (1u << 20) && bytes % 16 == 0, "bytes must be >= 1 MiB and a multiple of 16");
+    DevScope ds(device);
+    cudaStream_t st = nullptr;
+    GK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    ulonglong2* a = dalloc<ulonglong2>(bytes / 16, st);
+    unsigned long long* sink = dalloc<unsigned long long>(1, st);
+    GK_CUDA(cudaMemsetAsync(a, 1, bytes, st));
+    int sms = 0, per = 0;
+    GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_l2_read, 512, 0));
+    const unsigned grid = static_cast<unsigned>(std::max(1, per) * sms);
+    const int reps = 20;
+    cudaEvent_t e0, e1;
+    GK_CUDA(cudaEventCreate(&e0));
+    GK_CUDA(cudaEventCreate(&e1));
+    k_l2_read<<<grid, 512, 0, st>>>(a, bytes / 16, 2, sink);  // warm: the buffer L2-resident
+    float best = 1e30f;
+    for (int t = 0; t < 3; ++t) {
+      GK_CUDA(cudaEventRecord(e0, st));
+      k_l2_read<<<grid, 512, 0, st>>>(a, bytes / 16, reps, sink);
+      GK_CUDA(cudaEventRecord(e1, st));
+      GK_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      GK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    GK_CHECK_LAUNCH();
+    *gbs = static_cast<double>(bytes) * reps / (best * 1e-3) / 1e9;
+    dfree(a, st);
+    dfree(sink, st);
+    GK_CUDA(cudaStreamSynchronize(st));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+  });
+}
+
+int gk_bdl_knn_bounded_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k, const double* r2_dev,
+                              uint32_t* ids_dev, double* d2_dev) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(nq == 0 || (q_dev && r2_dev && ids_dev && d2_dev), "null buffer");
+    DevScope ds(h->device);
+    if (nq > 0) {
+      int* bad = dalloc<int>(1, h->st);
+      int hb = 0;
+      GK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), h->st));
+      k_check_radii<<<blocks_for(nq), 256, 0, h->st>>>(r2_dev, nq, bad);
+      GK_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      dfree(bad, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+      need(hb == 0, "every r2 must be a non-negative squared radius");
+    }
+    knn_device_impl(h, q_dev, nq, k, ids_dev, d2_dev, nullptr, r2_dev);
   });
 }
 
@@ -865,6 +973,102 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
                                 h->pst[1]));
         GK_CUDA(cudaMemcpyAsync(d2 + off * k, dd + off * k, m * k * sizeof(double), cudaMemcpyDeviceToHost, h->pst[1]));
       }
+      GK_CUDA(cudaEventRecord(ev_done, h->pst[1]));
+      GK_CUDA(cudaStreamWaitEvent(h->st, ev_done, 0));
+      dfree(dq, h->st);
+      dfree(di, h->st);
+      dfree(dd, h->st);
+      GK_CUDA(cudaStreamSynchronize(h->st));
+      return;
+    }
+    if (ts.count > 0 && nck > 1) {
+      // pageable host buffers (a std::vector caller): the same three-stage pipeline through a pinned
+      // staging ring -- host threads copy each 16 MiB block of queries into a ring slot that PCIe then
+      // reads, and copy each block of result rows out of the slot PCIe wrote, while the GPU works on the
+      // other slots and chunks.  Buffers that are already pinned are copied directly.
+      h->ensure_stage();
+      while (h->pev.size() < 2 * nck + 2) {
+        cudaEvent_t e;
+        GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->pev.push_back(e);
+      }
+      const int nth = std::max(1, std::min(16, host_threads()));
+      const bool pq = is_pinned(q), pi = is_pinned(ids), pd = is_pinned(d2);
+      cudaEvent_t ev_alloc = h->pev[0], ev_done = h->pev[1];
+      double* dq = dalloc<double>(nq * h->d, h->st);
+      std::uint32_t* di = dalloc<std::uint32_t>(nq * k, h->st);
+      double* dd = dalloc<double>(nq * k, h->st);
+      GK_CUDA(cudaEventRecord(ev_alloc, h->st));
+      GK_CUDA(cudaStreamWaitEvent(h->pst[0], ev_alloc, 0));
+      GK_CUDA(cudaStreamWaitEvent(h->pst[1], ev_alloc, 0));
+      int slot = 0;
+      bool used[gk_bdl::kStageSlots] = {};
+      // ring slot for the next transfer: wait until its previous transfer (and copy-out) finished
+      struct Out { int slot; void* dst; std::size_t n; };
+      std::vector<Out> pending;  // D2H blocks whose rows still have to reach the caller's memory
+      auto drain_one = [&] {
+        const Out o = pending.front();
+        pending.erase(pending.begin());
+        GK_CUDA(cudaEventSynchronize(h->stage_ev[o.slot]));
+        host_copy(o.dst, h->stage[o.slot], o.n, nth);
+      };
+      auto take_slot = [&]() {
+        const int s0 = slot;
+        slot = (slot + 1) % gk_bdl::kStageSlots;
+        for (std::size_t i = 0; i < pending.size(); ++i)
+          if (pending[i].slot == s0) {  // its rows must leave the slot first (in order)
+            while (!pending.empty() && pending.front().slot != s0) drain_one();
+            drain_one();
+            break;
+          }
+        if (used[s0]) GK_CUDA(cudaEventSynchronize(h->stage_ev[s0]));
+        used[s0] = true;
+        return s0;
+      };
+      auto h2d = [&](void* dst, const void* src, std::size_t n, bool pinned) {
+        if (pinned) {
+          GK_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, h->pst[0]));
+          return;
+        }
+        for (std::size_t off = 0; off < n; off += gk_bdl::kStageBytes) {
+          const std::size_t m = std::min(gk_bdl::kStageBytes, n - off);
+          const int sl = take_slot();
+          host_copy(h->stage[sl], static_cast<const char*>(src) + off, m, nth);
+          GK_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, h->stage[sl], m, cudaMemcpyHostToDevice, h->pst[0]));
+          GK_CUDA(cudaEventRecord(h->stage_ev[sl], h->pst[0]));
+        }
+      };
+      auto d2h = [&](void* dst, const void* src, std::size_t n, bool pinned) {
+        if (pinned) {
+          GK_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, h->pst[1]));
+          return;
+        }
+        for (std::size_t off = 0; off < n; off += gk_bdl::kStageBytes) {
+          const std::size_t m = std::min(gk_bdl::kStageBytes, n - off);
+          const int sl = take_slot();
+          GK_CUDA(cudaMemcpyAsync(h->stage[sl], static_cast<const char*>(src) + off, m, cudaMemcpyDeviceToHost, h->pst[1]));
+          GK_CUDA(cudaEventRecord(h->stage_ev[sl], h->pst[1]));
+          pending.push_back({sl, static_cast<char*>(dst) + off, m});
+          if (pending.size() >= gk_bdl::kStageSlots - 1) drain_one();
+        }
+      };
+      // queries in, kNN_L of each chunk as soon as its queries landed
+      for (std::uint64_t c = 0; c < nck; ++c) {
+        const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
+        h2d(dq + off * h->d, q + off * h->d, m * h->d * sizeof(double), pq);
+        GK_CUDA(cudaEventRecord(h->pev[2 + 2 * c], h->pst[0]));
+        GK_CUDA(cudaStreamWaitEvent(h->st, h->pev[2 + 2 * c], 0));
+        knn_launch(h->d, k, ts, dq + off * h->d, m, di + off * k, dd + off * k, nullptr, h->st, nullptr, nullptr);
+        GK_CUDA(cudaEventRecord(h->pev[3 + 2 * c], h->st));
+      }
+      // rows out, chunk by chunk as they become final
+      for (std::uint64_t c = 0; c < nck; ++c) {
+        const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
+        GK_CUDA(cudaStreamWaitEvent(h->pst[1], h->pev[3 + 2 * c], 0));
+        d2h(ids + off * k, di + off * k, m * k * sizeof(std::uint32_t), pi);
+        d2h(d2 + off * k, dd + off * k, m * k * sizeof(double), pd);
+      }
+      while (!pending.empty()) drain_one();
       GK_CUDA(cudaEventRecord(ev_done, h->pst[1]));
       GK_CUDA(cudaStreamWaitEvent(h->st, ev_done, 0));
       dfree(dq, h->st);

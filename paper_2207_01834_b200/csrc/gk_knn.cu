@@ -67,6 +67,10 @@ __device__ __forceinline__ void leaf_d2_pair(const double (&q)[D], const double*
   }
 }
 
+#ifndef GK_PAIRCHK
+#define GK_PAIRCHK 0  // 1: one min(da, db) <= kd test in front of the pair's two offers
+#endif
+
 // packed fp32x2 helpers (sm_100: FADD2/FMUL2 with directed rounding)
 __device__ __forceinline__ unsigned long long pk2(float a, float b) {
   return (static_cast<unsigned long long>(__float_as_uint(b)) << 32) | __float_as_uint(a);
@@ -120,7 +124,8 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
                                                         std::uint32_t* __restrict__ out_ids, double* __restrict__ out_d2,
                                                         unsigned long long* __restrict__ counters,
                                                         unsigned* __restrict__ tile_ctr,
-                                                        double* __restrict__ gheap) {
+                                                        double* __restrict__ gheap,
+                                                        const double* __restrict__ qbound) {
   constexpr int kWarps = warps_for<KT>();
   const int K = KT > 0 ? KT : k;  // k-buffer size (compile-time for the common k)
   __shared__ std::uint64_t s_stack[kWarps][kStack];
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   const int w = threadIdx.x >> 5;
   const unsigned ntiles = static_cast<unsigned>((nq + 31) / 32);
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0, c_ins = 0;
+  unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0, c_ins = 0, c_wlp = 0, c_wev = 0;
   float mdst[kStack];
 
   // persistent warps: each grabs the next 32-query tile (Morton order keeps
@@ -183,15 +188,18 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
     qhi2[j] = pk2(qhi[j], qhi[j]);
     if (kPairMode && kSmemQ) s_q[w][j * 32 + lane] = q[j];
   }
+  // (+inf, kNoPoint): KnnBuffer's initial bound; a bounded kNN starts from (r2, kNoPoint)
+  // sentinels instead, so only points with d2 <= r2 ever enter (ids < kNoPoint win the tie)
+  const double kinit = (qbound && active) ? qbound[orig] : kInf;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    cdv[j * CS] = kInf;  // (+inf, kNoPoint): KnnBuffer's initial bound
+    cdv[j * CS] = kinit;
     civ[j * CS] = GK_NO_POINT;
   }
-  double kd = kInf;                 // current k-th (d2, id) = heap root
+  double kd = kinit;                // current k-th (d2, id) = heap root
   std::uint32_t kid = GK_NO_POINT;
   // k-th distance rounded up to fp32 (the pruning threshold); inactive lanes never want anything
-  float kthf = active ? __int_as_float(0x7f800000) : -1.f;
+  float kthf = active ? __double2float_ru(kinit) : -1.f;
 
   // The k-buffer is a max-heap on (d2, id) in this lane's shared-memory column: the root
   // is the current k-th entry, an accepted point replaces it and sifts down (<= log2 K
@@ -221,6 +229,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
     if (d2 <= kd) {  // rare: lexicographic test against the k-th, then heap replace
       const std::uint32_t pid = s_ids[w][p];
       if (d2 < kd || pid < kid) {
+        if (COUNT && lane == __ffs(__activemask()) - 1) c_wev++;
         sift_down(d2, pid, K);
         kd = cdv[0];
         kid = civ[0];
@@ -259,8 +268,10 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
           for (std::uint32_t p = 0; p < c; p += 2) {
             double da, db;
             leaf_d2_pair<D>(q, s_pts[w], p, da, db);
-            offer(da, p);
-            offer(db, p + 1);
+            if (!GK_PAIRCHK || fmin(da, db) <= kd) {  // one test rejects both (the common case)
+              offer(da, p);
+              offer(db, p + 1);
+            }
           }
         } else if (m > 0) {
           // high D, few lanes need this leaf: spread the m x c needed (query, point) pairs
@@ -317,6 +328,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
         if (COUNT) {
           if (need) { c_leaves++; c_dists += c; }
           c_wl++;
+          c_wlp += c;
         }
       } else {
         const float4* nd = nodes + ref * (D + 1);
@@ -392,17 +404,18 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
 #pragma unroll
     for (int j = 0; j < K; ++j)
       if (j < k) {
-        out_ids[static_cast<std::uint64_t>(orig) * k + j] = civ[j * CS];
-        out_d2[static_cast<std::uint64_t>(orig) * k + j] = cdv[j * CS];
+        const std::uint32_t id = civ[j * CS];
+        out_ids[static_cast<std::uint64_t>(orig) * k + j] = id;
+        out_d2[static_cast<std::uint64_t>(orig) * k + j] = id == GK_NO_POINT ? kInf : cdv[j * CS];
       }
   }
   }  // tile loop
 
   if (COUNT) {
     const unsigned long long node_b = sizeof(TNode<D>), pt_b = 8 * D + 4;
-    unsigned long long v[4] = {c_nodes, c_leaves, c_dists, c_ins};
+    unsigned long long v[5] = {c_nodes, c_leaves, c_dists, c_ins, c_wev};
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 5; ++i)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
     if (lane == 0) {
@@ -414,6 +427,8 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
       atomicAdd(&counters[5], c_wn);
       atomicAdd(&counters[6], c_wl);
       atomicAdd(&counters[7], v[3]);
+      atomicAdd(&counters[8], c_wlp);
+      atomicAdd(&counters[9], v[4]);
     }
   }
 }
@@ -519,7 +534,7 @@ __global__ void k_curve_key(const double* __restrict__ Q, std::uint64_t nq, cons
 
 template <int D, int KT>
 void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, int k, std::uint32_t* ids,
-              double* d2, unsigned long long* ctr, cudaStream_t st) {
+              double* d2, unsigned long long* ctr, cudaStream_t st, const double* bound) {
   constexpr int kWarps = warps_for<KT>();
   const unsigned blocks = static_cast<unsigned>((nq + kWarps * 32 - 1) / (kWarps * 32));
   // per-lane top-K columns in shared memory (KT < 0: in a global scratch heap instead)
@@ -550,25 +565,25 @@ void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std
   unsigned* tile_ctr = nullptr;
   GK_CUDA(cudaMallocAsync(&tile_ctr, sizeof(unsigned), st));
   GK_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned), st));
-  if (ctr) k_knn<D, KT, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr, gheap);
-  else k_knn<D, KT, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr, gheap);
+  if (ctr) k_knn<D, KT, true><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr, gheap, bound);
+  else k_knn<D, KT, false><<<grid, kWarps * 32, smem, st>>>(ts, Q, perm, nq, k, ids, d2, ctr, tile_ctr, gheap, bound);
   GK_CUDA(cudaFreeAsync(tile_ctr, st));
   if (gheap) GK_CUDA(cudaFreeAsync(gheap, st));
 }
 
 template <int D>
 void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* perm, std::uint64_t nq, std::uint32_t* ids,
-              double* d2, unsigned long long* ctr, cudaStream_t st) {
-  if (k <= 1) launch_k<D, 1>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 2) launch_k<D, 2>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 4) launch_k<D, 4>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 5) launch_k<D, 5>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 8) launch_k<D, 8>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 10) launch_k<D, 10>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 16) launch_k<D, 16>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= 32) launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else if (k <= kMaxRuntimeK) launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st);
-  else launch_k<D, -1>(ts, Q, perm, nq, k, ids, d2, ctr, st);
+              double* d2, unsigned long long* ctr, cudaStream_t st, const double* bound) {
+  if (k <= 1) launch_k<D, 1>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 2) launch_k<D, 2>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 4) launch_k<D, 4>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 5) launch_k<D, 5>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 8) launch_k<D, 8>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 10) launch_k<D, 10>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 16) launch_k<D, 16>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 32) launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= kMaxRuntimeK) launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else launch_k<D, -1>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
 }
 
 template <int D>
@@ -958,22 +973,23 @@ void range_box_d(const TreeSet& ts, const double* lo, const double* hi, std::uin
 }  // namespace
 
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq, std::uint32_t* ids_dev,
-                double* d2_dev, gk_knn_counters* counters, cudaStream_t st, cudaEvent_t ev_k0, cudaEvent_t ev_k1) {
+                double* d2_dev, gk_knn_counters* counters, cudaStream_t st, cudaEvent_t ev_k0, cudaEvent_t ev_k1,
+                const double* bound) {
   if (nq == 0) return;
   if (nq >= 0xffffffffULL) throw Error(GK_ERR_INVALID, "kNN batch larger than 2^32-1 queries");
   std::uint32_t* perm = nullptr;
   GK_CUDA(cudaMallocAsync(&perm, nq * 4, st));
   unsigned long long* ctr = nullptr;
   if (counters) {
-    GK_CUDA(cudaMallocAsync(&ctr, 8 * sizeof(unsigned long long), st));
-    GK_CUDA(cudaMemsetAsync(ctr, 0, 8 * sizeof(unsigned long long), st));
+    GK_CUDA(cudaMallocAsync(&ctr, 10 * sizeof(unsigned long long), st));
+    GK_CUDA(cudaMemsetAsync(ctr, 0, 10 * sizeof(unsigned long long), st));
   }
   switch (d) {
 #define GK_D(DD)                                                   \
   case DD:                                                         \
     order_queries<DD>(q_dev, nq, perm, st);                        \
     if (ev_k0) GK_CUDA(cudaEventRecord(ev_k0, st));                \
-    launch_d<DD>(k, trees, q_dev, perm, nq, ids_dev, d2_dev, ctr, st); \
+    launch_d<DD>(k, trees, q_dev, perm, nq, ids_dev, d2_dev, ctr, st, bound); \
     if (ev_k1) GK_CUDA(cudaEventRecord(ev_k1, st));                \
     break;
     GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
@@ -982,7 +998,7 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
   }
   GK_CHECK_LAUNCH();
   if (counters) {
-    unsigned long long h[8];
+    unsigned long long h[10];
     GK_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, st));
     GK_CUDA(cudaStreamSynchronize(st));
     counters->node_bytes = h[0];
@@ -993,6 +1009,8 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
     counters->warp_nodes = h[5];
     counters->warp_leaves = h[6];
     counters->inserts = h[7];
+    counters->warp_leaf_points = h[8];
+    counters->warp_inserts = h[9];
     GK_CUDA(cudaFreeAsync(ctr, st));
   }
   GK_CUDA(cudaFreeAsync(perm, st));

@@ -5,7 +5,7 @@
 A=$1; B=$2; shift 2
 for r in 1 2; do
   for L in "$A" "$B"; do
-    GK_LIB=$L python bench.py --no-cpu-baseline "$@" 2>/dev/null | tail -n 1 | python -c "
+    GK_LIB=$L python bench.py --no-cpu-baseline --no-configs "$@" 2>/dev/null | tail -n 1 | python -c "
 import json,sys
 l=json.loads(sys.stdin.read())
 b=l.get('build') or {}

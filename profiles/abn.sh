@@ -4,7 +4,7 @@
 LIBS=$1; R=$2; shift 2
 for r in $(seq 1 $R); do
   for L in $LIBS; do
-    GK_LIB=$L python bench.py --no-cpu-baseline "$@" 2>/dev/null | tail -n 1 | python -c "
+    GK_LIB=$L python bench.py --no-cpu-baseline --no-configs "$@" 2>/dev/null | tail -n 1 | python -c "
 import json,sys
 l=json.loads(sys.stdin.read())
 b=l.get('build') or {}

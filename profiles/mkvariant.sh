@@ -14,5 +14,5 @@ for f in gk_knn gk_build; do
 done
 wait
 nvcc -shared -Wno-deprecated-gpu-targets -ccbin /usr/bin/g++ -o ab/$1/libgkbdl.so $L/gk_bdl.cu.o ab/$1/gk_build.cu.o \
-  ab/$1/gk_knn.cu.o $L/gk_gen.cpp.o -Xcompiler -fopenmp -lgomp
+  ab/$1/gk_knn.cu.o $L/gk_gen.cpp.o $L/gk_host.cpp.o -Xcompiler -fopenmp -lgomp
 echo ab/$1/libgkbdl.so

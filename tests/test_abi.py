@@ -4,6 +4,9 @@ import ctypes
 import os
 import re
 
+import numpy as np
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -66,3 +69,16 @@ def test_cli_usage_without_gpu(gk):
     assert os.path.exists(exe)
     assert subprocess.run([exe], capture_output=True).returncode == 1
     assert subprocess.run([exe, "frobnicate"], capture_output=True).returncode == 1
+
+
+def test_device_api_rejects_host_tensors():
+    """the torch-tensor checks of the device API run before any pointer crosses the ABI (no GPU needed)"""
+    import types
+    torch = pytest.importorskip("torch")
+    from paper_2207_01834_b200.bdltree import BDLTree
+    stub = types.SimpleNamespace(device=0)
+    with pytest.raises(ValueError, match="CUDA"):
+        BDLTree._dev(stub, torch.zeros((4, 3), dtype=torch.float64), "float64", (None, 3), "q_dev")
+    with pytest.raises(ValueError, match="CUDA"):
+        BDLTree._dev(stub, np.zeros((4, 3)), "float64", (None, 3), "q_dev")
+    assert BDLTree._dev(stub, None, "int32", (None,), "ids", optional=True) is None

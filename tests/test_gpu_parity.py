@@ -37,7 +37,9 @@ def assert_tree_equal(g, o, i):
     np.testing.assert_array_equal(gp[~dead], op[~dead])
     np.testing.assert_array_equal(gp[dead, 1:], op[dead, 1:])
     assert len(gn) == len(on), f"tree {i}: {len(gn)} vs {len(on)} nodes"
-    groot, oroot = int(g.info()["root_per_tree"][i]), o.tree_root(i)
+    # the buffer tree (i = -1) is rebuilt rather than collapsed: its root is slot 0
+    groot = int(g.info()["root_per_tree"][i]) if i >= 0 else (0 if len(gn) else -1)
+    oroot = o.tree_root(i)
     assert groot == oroot, f"tree {i}: root slot {groot} vs {oroot}"
     # nodes reachable from the root (Erase_S collapses splice nodes out; unreachable records are stale)
     reach, stack = [], [groot] if groot >= 0 else []
@@ -62,6 +64,8 @@ def assert_struct_equal(g, o, trees=True):
         for i in range(64):
             if gi["F"] >> i & 1:
                 assert_tree_equal(g, o, i)
+        if gi["buffer"]:
+            assert_tree_equal(g, o, -1)  # Build_S of the buffer (a-7): permutation + nodes bit-exact
 
 
 def run_script(gk, oracle, d, script, X=1024, leaf=16, heur=0, trees=True):
@@ -238,7 +242,7 @@ def _full_properties(P, Q, ids, d2, k):
     assert (np.diff(d2, axis=1) >= 0).all()
     same = np.diff(d2, axis=1) == 0
     assert (np.diff(ids.astype(np.int64), axis=1)[same] > 0).all()  # ties by ascending id
-    rows = np.random.default_rng(0).choice(len(Q), 20000, replace=False)
+    rows = np.random.default_rng(0).choice(len(Q), 20000, replace=False)  # d2 recomputed on a sample
     diff = Q[rows][:, None, :] - P[ids[rows].astype(np.int64)]
     rec = np.zeros(diff.shape[:2])
     for j in range(P.shape[1]):
@@ -248,22 +252,23 @@ def _full_properties(P, Q, ids, d2, k):
 
 
 @pytest.mark.slow
-def test_full_c2_sampled_against_oracle(gk, oracle):
-    """BASELINE config 2 at full size (10M points, 10M queries): properties on all rows, exact oracle
-    parity on 20k sampled rows (oracle BDL-tree over the same 10M points)."""
+def test_full_c2_every_row_against_oracle(gk, oracle):
+    """BASELINE config 2 at full size (10M points, 10M queries): every one of the 10M kNN rows against the
+    oracle BDL-tree over the same points (ids bit-exact, d2 within 1e-12), plus the size-independent
+    properties, the structure (F / buffer / live counts), the 8.4M-point tree and the buffer tree."""
     from paper_2207_01834_b200.configs import make_inputs
     d, script = make_inputs(2)
     P, (_, Q, k) = script[0][1], script[1]
     g = gk.BDLTree(3)
     g.insert(P)
     ids, d2 = g.knn(Q, k)
-    rows = _full_properties(P, Q, ids, d2, k)
+    _full_properties(P, Q, ids, d2, k)
     o = oracle.BDLTree(3)
     o.insert(P)
     assert_struct_equal(g, o, trees=False)
     assert_tree_equal(g, o, 13)  # the 8.4M-point tree: permutation + nodes bit-exact
-    oi, od = o.knn(Q[rows], k)
-    assert_knn_equal((ids[rows], d2[rows]), (oi, od), "C2 full sampled")
+    assert_tree_equal(g, o, -1)  # the buffer tree (640 points)
+    assert_knn_equal((ids, d2), o.knn(Q, k), "C2 full, every row")
 
 
 @pytest.mark.slow
@@ -275,35 +280,45 @@ def test_full_c1_self_queries(gk, oracle):
     g.insert(P)
     ids, d2 = g.knn(P, 5)
     assert np.array_equal(ids[:, 0], np.arange(len(P), dtype=np.uint32)) and (d2[:, 0] == 0).all()
-    rows = _full_properties(P, P, ids, d2, 5)
+    _full_properties(P, P, ids, d2, 5)
     o = oracle.BDLTree(2)
     o.insert(P)
     assert_struct_equal(g, o, trees=True)
-    assert_knn_equal((ids[rows], d2[rows]), o.knn(P[rows], 5), "C1 full sampled")
+    assert_knn_equal((ids, d2), o.knn(P, 5), "C1 full, every row")
 
 
-def test_pinned_pipelined_host_knn(gk):
-    """host API with pinned buffers takes the chunked copy/compute pipeline: results identical"""
+def test_host_knn_pipelines(gk):
+    """host API: pinned buffers take the chunked copy/compute pipeline, pageable ones the same pipeline
+    through the handle's pinned staging ring (blocks of 16 MiB, not a multiple of the row size here);
+    both identical to the device-resident kNN_L, for every chunk schedule"""
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(12)
     P = rng.random((300000, 3))
     Q = rng.random((2_600_000, 3))
     g = gk.BDLTree(3)
     g.insert(P)
-    ids0, d20 = g.knn(Q, 8)  # pageable: one-shot path
+    di = torch.empty((len(Q), 8), dtype=torch.int32, device="cuda")
+    dd = torch.empty((len(Q), 8), dtype=torch.float64, device="cuda")
+    g.knn_device(torch.from_numpy(Q).cuda(), 8, di, dd)
+    ids0, d20 = di.cpu().numpy().view(np.uint32), dd.cpu().numpy()
     Qp = torch.from_numpy(Q).pin_memory().numpy()
-    ids = torch.empty((len(Q), 8), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
-    d2 = torch.empty((len(Q), 8), dtype=torch.float64).pin_memory().numpy()
-    for chunks, ratio in (("4", "1"), ("5", "1.5"), ("3", "0.5"), ("40", "1")):  # schedule knobs
-        os.environ["GK_PIPE_CHUNKS"], os.environ["GK_PIPE_RATIO"] = chunks, ratio
-        ids.fill(0)
-        d2.fill(0)
-        try:
-            rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, len(Q), 8, ids.ctypes.data, d2.ctypes.data)
-        finally:
-            del os.environ["GK_PIPE_CHUNKS"], os.environ["GK_PIPE_RATIO"]
-        assert rc == 0
-        assert np.array_equal(ids, ids0) and np.array_equal(d2, d20), (chunks, ratio)
+    pinned = (torch.empty((len(Q), 8), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+              torch.empty((len(Q), 8), dtype=torch.float64).pin_memory().numpy())
+    pageable = (np.empty((len(Q), 8), np.uint32), np.empty((len(Q), 8), np.float64))
+    mixed = (pinned[0], pageable[1])
+    for qbuf, (ids, d2) in ((Qp, pinned), (Q, pageable), (Q, mixed), (Qp, pageable)):
+        for chunks, ratio in ((None, None), ("4", "1"), ("5", "1.5"), ("3", "0.5"), ("40", "1")):  # schedule knobs
+            if chunks:
+                os.environ["GK_PIPE_CHUNKS"], os.environ["GK_PIPE_RATIO"] = chunks, ratio
+            ids.fill(0)
+            d2.fill(0)
+            try:
+                rc = gk.lib().gk_bdl_knn(g._h, qbuf.ctypes.data, len(Q), 8, ids.ctypes.data, d2.ctypes.data)
+            finally:
+                os.environ.pop("GK_PIPE_CHUNKS", None)
+                os.environ.pop("GK_PIPE_RATIO", None)
+            assert rc == 0, gk.lib().gk_last_error()
+            assert np.array_equal(ids, ids0) and np.array_equal(d2, d20), (chunks, ratio)
 
 
 def test_bloom_filter(gk):
@@ -321,14 +336,13 @@ def test_bloom_filter(gk):
     assert g2.bloom_may_contain(0, np.array([[-0.0, 0.0, 1.0]])).all()  # -0 == +0 probes the same bits
 
 
-def _sampled_script_parity(gk, oracle, cfg, nsample=20000, trees=True):
-    """Full-size BASELINE script on both sides: structure (F, buffer, live counts, every static tree's
-    permutation/tombstones/nodes) bit-exact after every operation, kNN rows exact on a seeded sample."""
+def _script_parity(gk, oracle, cfg, trees=True):
+    """Full-size BASELINE script on both sides: structure (F, buffer, live counts, every static tree's and the
+    buffer tree's permutation/tombstones/nodes) bit-exact after every operation, every kNN row exact."""
     from paper_2207_01834_b200.configs import make_inputs
     d, script = make_inputs(cfg)
     g = gk.BDLTree(d)
     o = oracle.BDLTree(d)
-    rng = np.random.default_rng(cfg)
     for step, op in enumerate(script):
         if op[0] == "insert":
             g.insert(op[1]); o.insert(op[1])
@@ -338,25 +352,22 @@ def _sampled_script_parity(gk, oracle, cfg, nsample=20000, trees=True):
             assert_struct_equal(g, o, trees)
         else:
             Q, k = op[1], op[2]
-            ids, d2 = g.knn(Q, k)
-            rows = np.sort(rng.choice(len(Q), min(nsample, len(Q)), replace=False))
-            assert_knn_equal((ids[rows], d2[rows]), o.knn(Q[rows], k), f"config {cfg} step {step}")
-            assert (np.diff(d2, axis=1) >= 0).all()
+            assert_knn_equal(g.knn(Q, k), o.knn(Q, k), f"config {cfg} step {step}, every row")
 
 
 @pytest.mark.slow
-def test_full_c3_sampled(gk, oracle):
-    _sampled_script_parity(gk, oracle, 3)
+def test_full_c3_every_row(gk, oracle):
+    _script_parity(gk, oracle, 3)
 
 
 @pytest.mark.slow
-def test_full_c4_sampled(gk, oracle):
-    _sampled_script_parity(gk, oracle, 4, nsample=5000)
+def test_full_c4_every_row(gk, oracle):
+    _script_parity(gk, oracle, 4)
 
 
 @pytest.mark.slow
-def test_full_c5_sampled(gk, oracle):
-    _sampled_script_parity(gk, oracle, 5)
+def test_full_c5_every_row(gk, oracle):
+    _script_parity(gk, oracle, 5)
 
 
 @pytest.mark.slow
@@ -379,3 +390,54 @@ def test_heavy_duplicates_at_scale(gk, oracle):
     script = [("insert", P), ("knn", sites[:500], 16), ("erase", sites[:300]), ("knn", sites[:500], 16),
               ("insert", P[:5000]), ("knn", rng.random((2000, 2)), 7)]
     run_script(gk, oracle, 2, script, X=4096)
+
+
+def test_bounded_knn(gk, oracle):
+    """radius-bounded kNN_L: row i = the exact kNN row cut at d2 <= r2[i] (inclusive), padded with
+    (NO_POINT, +inf); r2 = +inf is plain kNN_L, r2 = 0 keeps only coincident points"""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(31)
+    P = np.round(rng.random((40000, 3)) * 200) / 200  # duplicates: ties at the radius
+    Q = np.concatenate([rng.random((3000, 3)), P[:500]])
+    k = 10
+    o = oracle.BDLTree(3)
+    o.insert(P)
+    ei, ed = o.knn(Q, k)
+    r2 = ed[np.arange(len(Q)), rng.integers(0, k, len(Q))].copy()  # a radius through some row entry
+    r2[::7] = np.inf
+    r2[3::7] = 0.0
+    r2[5::7] *= 0.5
+    g = gk.BDLTree(3)
+    g.insert(P)
+    ids = torch.empty((len(Q), k), dtype=torch.int32, device="cuda")
+    d2 = torch.empty((len(Q), k), dtype=torch.float64, device="cuda")
+    g.knn_bounded_device(torch.from_numpy(Q).cuda(), k, torch.from_numpy(r2).cuda(), ids, d2)
+    gi, gd = ids.cpu().numpy().view(np.uint32), d2.cpu().numpy()
+    keep = ed <= r2[:, None]
+    wi = np.where(keep, ei, gk.NO_POINT).astype(np.uint32)
+    wd = np.where(keep, ed, np.inf)
+    assert np.array_equal(gi, wi) and np.array_equal(gd, wd)
+    bad = torch.from_numpy(r2).cuda()
+    bad[1] = -1.0
+    with pytest.raises(ValueError):
+        g.knn_bounded_device(torch.from_numpy(Q).cuda(), k, bad, ids, d2)
+
+
+def test_device_tensor_validation(gk):
+    """the device API refuses tensors whose raw pointers would be misread: host tensors, wrong dtypes,
+    strided views, wrong shapes"""
+    torch = pytest.importorskip("torch")
+    g = gk.BDLTree(3)
+    g.insert(np.random.default_rng(1).random((5000, 3)))
+    q = torch.rand((100, 3), dtype=torch.float64, device="cuda")
+    ids = torch.empty((100, 4), dtype=torch.int32, device="cuda")
+    d2 = torch.empty((100, 4), dtype=torch.float64, device="cuda")
+    g.knn_device(q, 4, ids, d2)
+    for args in ((q.cpu(), 4, ids, d2), (q, 4, ids.long(), d2), (q, 4, ids, d2.float()), (q.t().contiguous().t(), 4, ids, d2),
+                 (q, 5, ids, d2), (q[:, :2], 4, ids, d2), (q.float(), 4, ids, d2), (q, 4, ids[:50], d2)):
+        with pytest.raises(ValueError):
+            g.knn_device(*args)
+    with pytest.raises(ValueError):
+        g.insert_device(torch.rand((10, 3), dtype=torch.float64))
+    with pytest.raises(ValueError):
+        g.range_device(q, 0.01, torch.zeros(101, dtype=torch.int64), None, None, 0)
