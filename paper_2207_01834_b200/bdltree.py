@@ -58,6 +58,16 @@ _u64 = C.c_uint64
 _lib = None
 
 
+def _bind(L, name, argtypes):
+    """argtypes of one C-ABI entry point; a missing symbol is an error unless GK_LIB points at another
+    build (A/B experiments against older builds that predate an entry point)"""
+    try:
+        getattr(L, name).argtypes = argtypes
+    except AttributeError:
+        if not os.environ.get("GK_LIB"):
+            raise
+
+
 def lib():
     """Load libgkbdl.so (build it first if it is missing and nvcc is present)."""
     global _lib
@@ -68,40 +78,40 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.gk_last_error.restype = C.c_char_p
         L.gk_version.restype = C.c_char_p
-        L.gk_bdl_create.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(_P)]
-        L.gk_bdl_destroy.argtypes = [_P]
-        L.gk_bdl_insert.argtypes = [_P, _P, _u64]
-        L.gk_bdl_insert_device.argtypes = [_P, _P, _u64]
-        L.gk_bdl_erase.argtypes = [_P, _P, _u64, C.POINTER(_u64)]
-        L.gk_bdl_erase_device.argtypes = [_P, _P, _u64, C.POINTER(_u64)]
-        L.gk_bdl_knn.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
-        L.gk_bdl_knn_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P]
-        L.gk_bdl_knn_bounded_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, _P]
-        L.gk_bdl_knn_counted_device.argtypes = [_P, _P, _u64, C.c_int, _P, _P, C.POINTER(KnnCounters)]
-        L.gk_bdl_range_count.argtypes = [_P, _P, _u64, C.c_double, _P]
-        L.gk_bdl_range.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64]
-        L.gk_bdl_range_device.argtypes = [_P, _P, _u64, C.c_double, _P, _P, _P, _u64, C.POINTER(_u64)]
-        L.gk_bdl_range_radii_count.argtypes = [_P, _P, _u64, _P, _P]
-        L.gk_bdl_range_radii.argtypes = [_P, _P, _u64, _P, _P, _P, _P, _u64]
-        L.gk_bdl_range_radii_device.argtypes = [_P, _P, _u64, _P, _P, _P, _P, _u64, C.POINTER(_u64)]
-        L.gk_bdl_range_box_count.argtypes = [_P, _P, _P, _u64, _P]
-        L.gk_bdl_range_box.argtypes = [_P, _P, _P, _u64, _P, _P, _u64]
-        L.gk_bdl_range_box_device.argtypes = [_P, _P, _P, _u64, _P, _P, _u64, C.POINTER(_u64)]
-        L.gk_bdl_knn_graph.argtypes = [_P, C.c_int, _P, _P, _P]
-        L.gk_bdl_knn_graph_device.argtypes = [_P, C.c_int, _P, _P, _P]
-        L.gk_bdl_info_get.argtypes = [_P, C.POINTER(_Info)]
-        L.gk_bdl_tree_export.argtypes = [_P, C.c_int, _P, _P, _P, C.POINTER(_u64), C.POINTER(_u64)]
-        L.gk_bdl_bloom_query.argtypes = [_P, C.c_int, _P, _u64, _P]
+        _bind(L, "gk_bdl_create", [C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.POINTER(_P)])
+        _bind(L, "gk_bdl_destroy", [_P])
+        _bind(L, "gk_bdl_insert", [_P, _P, _u64])
+        _bind(L, "gk_bdl_insert_device", [_P, _P, _u64])
+        _bind(L, "gk_bdl_erase", [_P, _P, _u64, C.POINTER(_u64)])
+        _bind(L, "gk_bdl_erase_device", [_P, _P, _u64, C.POINTER(_u64)])
+        _bind(L, "gk_bdl_knn", [_P, _P, _u64, C.c_int, _P, _P])
+        _bind(L, "gk_bdl_knn_device", [_P, _P, _u64, C.c_int, _P, _P])
+        _bind(L, "gk_bdl_knn_bounded_device", [_P, _P, _u64, C.c_int, _P, _P, _P])
+        _bind(L, "gk_bdl_knn_counted_device", [_P, _P, _u64, C.c_int, _P, _P, C.POINTER(KnnCounters)])
+        _bind(L, "gk_bdl_range_count", [_P, _P, _u64, C.c_double, _P])
+        _bind(L, "gk_bdl_range", [_P, _P, _u64, C.c_double, _P, _P, _P, _u64])
+        _bind(L, "gk_bdl_range_device", [_P, _P, _u64, C.c_double, _P, _P, _P, _u64, C.POINTER(_u64)])
+        _bind(L, "gk_bdl_range_radii_count", [_P, _P, _u64, _P, _P])
+        _bind(L, "gk_bdl_range_radii", [_P, _P, _u64, _P, _P, _P, _P, _u64])
+        _bind(L, "gk_bdl_range_radii_device", [_P, _P, _u64, _P, _P, _P, _P, _u64, C.POINTER(_u64)])
+        _bind(L, "gk_bdl_range_box_count", [_P, _P, _P, _u64, _P])
+        _bind(L, "gk_bdl_range_box", [_P, _P, _P, _u64, _P, _P, _u64])
+        _bind(L, "gk_bdl_range_box_device", [_P, _P, _P, _u64, _P, _P, _u64, C.POINTER(_u64)])
+        _bind(L, "gk_bdl_knn_graph", [_P, C.c_int, _P, _P, _P])
+        _bind(L, "gk_bdl_knn_graph_device", [_P, C.c_int, _P, _P, _P])
+        _bind(L, "gk_bdl_info_get", [_P, C.POINTER(_Info)])
+        _bind(L, "gk_bdl_tree_export", [_P, C.c_int, _P, _P, _P, C.POINTER(_u64), C.POINTER(_u64)])
+        _bind(L, "gk_bdl_bloom_query", [_P, C.c_int, _P, _u64, _P])
         L.gk_bdl_stream.restype = _P
-        L.gk_bdl_stream.argtypes = [_P]
-        L.gk_bdl_sync.argtypes = [_P]
-        L.gk_bdl_last_knn_ms.argtypes = [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)]
-        L.gk_bdl_last_build_ms.argtypes = [_P, C.POINTER(C.c_float), C.POINTER(_u64)]
-        L.gk_diag_l2_read_gbs.argtypes = [C.c_int, _u64, C.POINTER(C.c_double)]
-        L.gk_gen_uniform.argtypes = [_u64, C.c_int, _u64, _P]
-        L.gk_gen_mixture.argtypes = [_u64, C.c_int, _u64, C.c_int, C.c_double, _P]
-        L.gk_gen_walk.argtypes = [_u64, _u64, _u64, _P]
-        L.gk_sample_without_replacement.argtypes = [_u64, _u64, _u64, _P]
+        _bind(L, "gk_bdl_stream", [_P])
+        _bind(L, "gk_bdl_sync", [_P])
+        _bind(L, "gk_bdl_last_knn_ms", [_P, C.POINTER(C.c_float), C.POINTER(C.c_float)])
+        _bind(L, "gk_bdl_last_build_ms", [_P, C.POINTER(C.c_float), C.POINTER(_u64)])
+        _bind(L, "gk_diag_l2_read_gbs", [C.c_int, _u64, C.POINTER(C.c_double)])
+        _bind(L, "gk_gen_uniform", [_u64, C.c_int, _u64, _P])
+        _bind(L, "gk_gen_mixture", [_u64, C.c_int, _u64, C.c_int, C.c_double, _P])
+        _bind(L, "gk_gen_walk", [_u64, _u64, _u64, _P])
+        _bind(L, "gk_sample_without_replacement", [_u64, _u64, _u64, _P])
         _lib = L
     return _lib
 

@@ -254,7 +254,6 @@ struct gk_bdl {
   std::uint32_t* buf_ids = nullptr;
   std::uint64_t buf_n = 0;
   DevTree buf_tree;
-  std::uint32_t* buf_src = nullptr;  // buffer-tree position -> arrival index
   std::uint64_t next_id = 0;
   float knn_ms = 0.f, knn_total_ms = 0.f, build_ms = 0.f;
   double knn_ns_q = 0.0;  // device ns per query of the last one-shot kNN_L (k = knn_ns_k): e2e chunk planning
@@ -274,6 +273,27 @@ struct gk_bdl {
   cudaEvent_t stage_ev[kStageSlots] = {};
 
   std::uint64_t bstride() const { return 2ULL * X; }
+
+  // The memory pool (release threshold: never) only grows, and growing it maps new physical memory
+  // inside whichever cudaMallocAsync finds it short -- milliseconds each, erratic, on the host.  Before
+  // an operation that allocates `bytes`, grow it once, in one piece, to have that much free.
+  void ensure_pool(std::size_t bytes) {
+    cudaMemPool_t pool;
+    GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    std::uint64_t reserved = 0, used = 0;
+    GK_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    GK_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    const std::uint64_t free_b = reserved > used ? reserved - used : 0;
+    if (free_b >= bytes) return;
+    const std::size_t grow = bytes + bytes / 4;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, grow, st) != cudaSuccess) {  // out of memory here is not an error yet: the
+      cudaGetLastError();                                // operation itself may still fit
+      return;
+    }
+    GK_CUDA(cudaFreeAsync(p, st));
+    GK_CUDA(cudaStreamSynchronize(st));  // the free completed: every stream may reuse the block
+  }
 
   void ensure_stage() {
     if (stage[0]) return;
@@ -312,15 +332,17 @@ struct gk_bdl {
     PhaseTrace tr;
     tr.st = st;
     free_tree(buf_tree, st);
-    dfree(buf_src, st);
     if (buf_n == 0) return;
-    // Build_S over the buffer with its real ids (object-median ties break by id, as in every static
-    // tree), then buf_src[pos] = arrival index of the point at tree position pos, for erase compaction:
-    // ids are unique, so sort (id, arrival) and binary-search each tree id.
+    // Build_S over the buffer with its real ids (object-median ties break by id, as in every static tree)
     build_begin(scratch, d, static_cast<int>(leaf), heuristic, buf_coords, bstride(), buf_ids, buf_n, buf_tree, st);
     tr("  buffer: k_build done");
     build_finish(scratch);
     tr("  buffer: emitted");
+  }
+
+  // src[pos] = arrival index of the buffer point at buffer-tree position pos (erase compaction only):
+  // ids are unique, so sort (id, arrival) by id and binary-search each tree id
+  std::uint32_t* buffer_src_map() {
     std::uint32_t* iota = dalloc<std::uint32_t>(buf_n, st);
     std::uint32_t* skeys = dalloc<std::uint32_t>(buf_n, st);
     std::uint32_t* svals = dalloc<std::uint32_t>(buf_n, st);
@@ -329,13 +351,14 @@ struct gk_bdl {
     GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, buf_ids, skeys, iota, svals, static_cast<int>(buf_n), 0, 32, st));
     void* tmp = dalloc<char>(tb, st);
     GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, buf_ids, skeys, iota, svals, static_cast<int>(buf_n), 0, 32, st));
-    buf_src = dalloc<std::uint32_t>(buf_n, st);
-    k_map_src<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_n, skeys, svals, buf_src);
+    std::uint32_t* src = dalloc<std::uint32_t>(buf_n, st);
+    k_map_src<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.ids, buf_n, skeys, svals, src);
     GK_CHECK_LAUNCH();
     dfree(tmp, st);
     dfree(iota, st);
     dfree(skeys, st);
     dfree(svals, st);
+    return src;
   }
 
   // Insert_L of device SoA points (stride sp) with their ids.
@@ -362,6 +385,17 @@ struct gk_bdl {
     std::uint64_t pool_n = drained + bulk;
     for (int i = 0; i < 64; ++i)
       if (destroyed >> i & 1ULL) pool_n += statics[i].live;
+    {
+      std::size_t need = pool_n * (8 * d + 4) + build_bytes(d, buf_n + X);
+      std::uint64_t left = pool_n;
+      for (int i = 63; i >= 0; --i)
+        if (built >> i & 1ULL) {
+          const std::uint64_t c = std::min<std::uint64_t>(static_cast<std::uint64_t>(X) << i, left);
+          need += build_bytes(d, c);
+          left -= c;
+        }
+      ensure_pool(need);
+    }
     double* pool = dalloc<double>(pool_n * d, st);
     std::uint32_t* pool_ids = dalloc<std::uint32_t>(pool_n, st);
     tr("pool allocated", static_cast<long long>(pool_n));
@@ -537,7 +571,9 @@ struct gk_bdl {
         std::vector<std::uint32_t> ones(buf_n + 1, 1u);
         ones[buf_n] = 0;
         GK_CUDA(cudaMemcpyAsync(flags, ones.data(), (buf_n + 1) * 4, cudaMemcpyHostToDevice, st));
-        k_buffer_dead<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.coords, buf_src, buf_n, flags);
+        std::uint32_t* src = buffer_src_map();
+        k_buffer_dead<<<blocks_for(buf_n), 256, 0, st>>>(buf_tree.coords, src, buf_n, flags);
+        dfree(src, st);
         scan(flags, pos, buf_n + 1);
         double* nc = dalloc<double>(bstride() * d, st);
         std::uint32_t* ni = dalloc<std::uint32_t>(bstride(), st);
@@ -671,7 +707,6 @@ int gk_bdl_destroy(gk_bdl* h) {
     DevScope ds(h->device);
     for (auto& t : h->statics) free_tree(t, h->st);
     free_tree(h->buf_tree, h->st);
-    dfree(h->buf_src, h->st);
     dfree(h->buf_coords, h->st);
     dfree(h->buf_ids, h->st);
     if (h->cub_tmp) cudaFreeAsync(h->cub_tmp, h->st);

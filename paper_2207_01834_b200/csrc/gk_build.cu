@@ -1088,6 +1088,25 @@ int grid_wanted_d(std::uint64_t n) {
   return static_cast<int>(std::min<std::uint64_t>(capacity_d<D>(), std::max<std::uint64_t>(1, n / 4096)));
 }
 
+// device scratch of one build (every array build_begin_d carves out of it, 256-byte aligned)
+template <int D>
+std::size_t scratch_bytes(std::uint64_t n, std::uint64_t cap_chunks, int G) {
+  const std::uint64_t cap = 2 * n - 1, cap_level = std::min<std::uint64_t>(cap, n);
+  return 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) + (cap_level + 1) * 4 * 5 +
+         cap_chunks * 4 * 3 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 + C_COUNT * 4 + kSelCap * sizeof(SelState) +
+         kSelCap * 256 * 4 + (2 * G + 2) * 4 + 4 * (cap + 1) + 40 * 256;
+}
+
+// upper bound of the device memory one build allocates: its scratch (at the smallest chunk size) plus
+// the tree it leaves behind (coordinates, ids, canonical + traversal nodes, topology, ranks)
+template <int D>
+std::size_t build_bytes_d(std::uint64_t n) {
+  if (n == 0) return 0;
+  const std::uint64_t cap = 2 * n - 1;
+  const std::size_t tree = n * (8 * D + 4) + cap * (sizeof(gk_canon_node) + 12 + 4) + (cap / 2 + 1) * sizeof(TNode<D>);
+  return scratch_bytes<D>(n, n / 32 + std::min<std::uint64_t>(cap, n) + 2, capacity_d<D>()) + tree + 8 * 4096;
+}
+
 template <int D>
 void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
                    const std::uint32_t* src_ids, std::uint64_t n, DevTree& T, cudaStream_t st, int max_grid) {
@@ -1123,10 +1142,7 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   a.src = src;
   a.src_stride = src_stride;
   a.src_ids = src_ids;
-  const std::size_t need = 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) +
-                           (cap_level + 1) * 4 * 5 + cap_chunks * 4 * 3 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 +
-                           C_COUNT * 4 + kSelCap * sizeof(SelState) + kSelCap * 256 * 4 + (2 * G + 2) * 4 + 4 * (cap + 1) +
-                           40 * 256;
+  const std::size_t need = scratch_bytes<D>(n, cap_chunks, G);
   char* base = sc.reserve(need, st);
   std::size_t used = 0;
   auto take = [&](std::size_t bytes) -> char* {
@@ -1252,6 +1268,19 @@ int build_capacity(int d) {
     case 6: return capacity_d<6>();
     case 7: return capacity_d<7>();
     case 8: return capacity_d<8>();
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+}
+
+std::size_t build_bytes(int d, std::uint64_t n) {
+  switch (d) {
+    case 2: return build_bytes_d<2>(n);
+    case 3: return build_bytes_d<3>(n);
+    case 4: return build_bytes_d<4>(n);
+    case 5: return build_bytes_d<5>(n);
+    case 6: return build_bytes_d<6>(n);
+    case 7: return build_bytes_d<7>(n);
+    case 8: return build_bytes_d<8>(n);
     default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
   }
 }

@@ -159,6 +159,8 @@ void build_begin(BuildScratch& sc, int d, int leaf, int heuristic, const double*
                  const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st, int max_grid = 0);
 // co-resident blocks of the BuildvEB_S kernel for dimension d (its largest cooperative grid)
 int build_capacity(int d);
+// upper bound of the device bytes one build of n points allocates (scratch + the resulting tree)
+std::size_t build_bytes(int d, std::uint64_t n);
 // the grid a build of n points asks for when it runs alone
 int build_grid_wanted(int d, std::uint64_t n);
 void build_finish(BuildScratch& sc);

@@ -12,6 +12,8 @@ from paper_2207_01834_b200 import configs  # noqa: E402
 
 d, script = configs.make_inputs(4, 1.0)
 ins = [torch.from_numpy(op[1]).cuda() for op in script if op[0] == "insert"]
+qs = [torch.from_numpy(op[1]).cuda() for op in script if op[0] == "knn"]
+with_knn = os.environ.get("KNN") == "1"  # interleave the config's kNN_L batches (as bench.py replays it)
 reps = int(os.environ.get("REPS", "2"))
 for rep in range(reps):
     g = gk.BDLTree(d)
@@ -24,9 +26,13 @@ for rep in range(reps):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         tot += dt
+        if with_knn:
+            ids = torch.empty((qs[b].shape[0], 10), dtype=torch.int32, device="cuda")
+            d2 = torch.empty((qs[b].shape[0], 10), dtype=torch.float64, device="cuda")
+            g.knn_device(qs[b], 10, ids, d2)
         F1 = g.info()["F"]
         built = [i for i in range(64) if (F1 >> i & 1) and not (F0 >> i & 1)]
-        if rep:
+        if rep or os.environ.get("ALL"):
             print(f"batch {b}: {1e3 * dt:.3f} ms, build {g.last_build_ms()}, new trees {built}", file=sys.stderr, flush=True)
     print(f"rep {rep}: all inserts {1e3 * tot:.2f} ms", file=sys.stderr, flush=True)
     g.close()
