@@ -11,9 +11,11 @@
 int main() {
   std::vector<std::array<double, 3>> P(100000);
   if (gk_gen_uniform(P.size(), 3, 2, P[0].data()) != GK_OK) return 1;
-  geokit::bdltree::BDLTree<3> tree;           // X = 1024, leaf 16, spatial median
-  tree.insert(P);                             // bdl_build
-  auto nn = tree.knn(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 4), 3);
+  namespace bdl = geokit::bdltree;
+  // SPEC.md's free functions: bdl_build / bdl_insert / bdl_erase / bdl_knn (X = 1024, leaf 16, spatial median)
+  auto tree = bdl::bdl_build<3>(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 60000));
+  bdl::bdl_insert(tree, std::vector<std::array<double, 3>>(P.begin() + 60000, P.end()));
+  auto nn = bdl::bdl_knn(tree, std::vector<std::array<double, 3>>(P.begin(), P.begin() + 4), 3);
   for (auto& row : nn) {
     for (auto& [d2, id] : row) std::printf("(%u, %.3g) ", id, d2);
     std::printf("\n");
@@ -25,7 +27,7 @@ int main() {
   std::printf("per-query range rows %zu %zu\n", ball2[0].size(), ball2[1].size());
   std::vector<std::array<double, 3>> lo{{0.4, 0.4, 0.4}}, hi{{0.45, 0.45, 0.45}};
   std::printf("box rows %zu\n", tree.range_box(lo, hi)[0].size());  // orthogonal range search
-  const unsigned long long erased = tree.erase(std::vector<std::array<double, 3>>(P.begin(), P.begin() + 10));
+  const unsigned long long erased = bdl::bdl_erase(tree, std::vector<std::array<double, 3>>(P.begin(), P.begin() + 10));
   auto graph = tree.knn_graph(2);  // k-NN graph over the live points
   std::printf("graph rows %zu, first row of id %u\n", graph.size(), graph[0].first);
   std::printf("erased %llu, live %llu\n", erased, (unsigned long long)tree.size());

@@ -32,7 +32,7 @@ namespace detail {
 inline void check(int rc) {
   if (rc == GK_OK) return;
   const std::string msg = gk_last_error();
-  if (rc == GK_ERR_INVALID) throw std::invalid_argument(msg);
+  if (rc == GK_ERR_INVALID || rc == GK_ERR_CAPACITY) throw std::invalid_argument(msg);
   if (rc == GK_ERR_UNSUPPORTED) throw std::invalid_argument(msg);
   if (rc == GK_ERR_LOGIC) throw std::logic_error(msg);
   throw std::runtime_error(msg);
@@ -59,6 +59,14 @@ class BDLTree {
   BDLTree(const BDLTree&) = delete;
   BDLTree& operator=(const BDLTree&) = delete;
   BDLTree(BDLTree&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  BDLTree& operator=(BDLTree&& o) noexcept {
+    if (this != &o) {
+      gk_bdl_destroy(h_);
+      h_ = o.h_;
+      o.h_ = nullptr;
+    }
+    return *this;
+  }
 
   /// bdl_insert (Insert_L, Alg. 3); on an empty tree this is bdl_build.
   template <class PointSet>
@@ -177,5 +185,34 @@ class BDLTree {
  private:
   gk_bdl* h_ = nullptr;
 };
+
+// ---- SPEC.md's free-function interface of the bdltree module, over the class above.
+
+/// bdl_build(P) -> BDLTree: bdl_insert(P) on an empty structure.
+template <int D, class PointSet>
+BDLTree<D> bdl_build(const PointSet& P, std::uint32_t buffer_size = 1024, std::uint32_t leaf_size = 16,
+                     Heuristic h = Heuristic::SpatialMedian, int device = 0) {
+  BDLTree<D> t(buffer_size, leaf_size, h, device);
+  t.insert(P);
+  return t;
+}
+
+/// bdl_insert(tree, P) (Algorithm 3).
+template <int D, class PointSet>
+void bdl_insert(BDLTree<D>& tree, const PointSet& P) {
+  tree.insert(P);
+}
+
+/// bdl_erase(tree, P) (Algorithm 4); also returns the number of points removed.
+template <int D, class PointSet>
+std::uint64_t bdl_erase(BDLTree<D>& tree, const PointSet& P) {
+  return tree.erase(P);
+}
+
+/// bdl_knn(tree, S, k) -> per-query k nearest, each row as KnnBuffer::extract().
+template <int D, class PointSet>
+std::vector<std::vector<Entry>> bdl_knn(BDLTree<D>& tree, const PointSet& S, int k) {
+  return tree.knn(S, k);
+}
 
 }  // namespace geokit::bdltree

@@ -6,9 +6,9 @@
  * and the shipped headers' conventions imply:
  *
  *   gk_bdl_create   <- BDLTree type, X = 1024, leaf 16
- *   gk_bdl_insert   <- bdl_build / bdl_insert (Insert_L)     SPEC.md:563-580, PAPER.md:1229-1248 (Alg. 3)
- *   gk_bdl_erase    <- bdl_erase (Erase_L)                   SPEC.md:581-589, PAPER.md:1255-1269 (Alg. 4)
- *   gk_bdl_knn      <- bdl_knn (kNN_L) over knn_batch/kNN_S  SPEC.md:590-597, 505-513; PAPER.md:1206-1224, 1285-1287
+ *   gk_bdl_insert   <- bdl_build / bdl_insert (Insert_L)     SPEC.md:563-580, PAPER.md:1178-1195 (Alg. 3)
+ *   gk_bdl_erase    <- bdl_erase (Erase_L)                   SPEC.md:581-589, PAPER.md:1203-1216 (Alg. 4)
+ *   gk_bdl_knn      <- bdl_knn (kNN_L) over knn_batch/kNN_S  SPEC.md:590-597, 505-513; PAPER.md:1153-1160, 1231-1233
  *                      rows = KnnBuffer::extract() order     geokit/kdtree/knn_buffer.hpp:42-46 (sorted by (d2, id))
  *   gk_bdl_range    <- kd-tree range search (ball / box)     PAPER.md:188-190, 204, 230 (
  *                      SPEC.md:628 leaves it out of geokit's scope)
@@ -45,7 +45,8 @@ enum gk_status {
   GK_ERR_INVALID = 1,     /* std::invalid_argument in the reference */
   GK_ERR_CUDA = 2,        /* CUDA runtime failure (message in gk_last_error) */
   GK_ERR_UNSUPPORTED = 3, /* e.g. k > GK_MAX_K */
-  GK_ERR_LOGIC = 4        /* std::logic_error: id space exhausted, bad handle state */
+  GK_ERR_LOGIC = 4,       /* std::logic_error: id space exhausted, bad handle state */
+  GK_ERR_CAPACITY = 5     /* range search: more rows than `capacity`; offsets were written, call again */
 };
 
 enum gk_heuristic { GK_SPATIAL_MEDIAN = 0, GK_OBJECT_MEDIAN = 1 };
@@ -124,7 +125,8 @@ int gk_bdl_knn_counted_device(gk_bdl* h, const double* q_dev, uint64_t nq, int k
  * gk_bdl_range_count: counts[i] = number of rows of query i.
  * gk_bdl_range: offsets[nq + 1] = exclusive prefix sums of the counts (offsets[nq] = total), rows of
  * query i at [offsets[i], offsets[i+1]) of ids / d2, sorted by (d2, id).  ids and d2 hold `capacity`
- * rows; a larger result fails with GK_ERR_INVALID after writing offsets (call again with room).
+ * rows; a larger result fails with GK_ERR_CAPACITY after writing offsets (call again with room);
+ * any other failure (GK_ERR_INVALID for a NaN / negative r2, ...) leaves offsets unwritten.
  * The _device variant takes device pointers and reports the total in *total. */
 int gk_bdl_range_count(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* counts);
 int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* offsets, uint32_t* ids, double* d2,

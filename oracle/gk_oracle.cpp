@@ -6,10 +6,10 @@
 // CUDA path is compared against, and the "reference CPU path" timed beside it.
 //
 // It is a restatement, in plain C++17 + OpenMP (TBB/Eigen are absent here), of
-//   * PAPER.md Alg. 1 BuildvEB_S                 (/root/reference/PAPER.md:1110-1127)
-//   * PAPER.md Alg. 2 Erase_S                    (PAPER.md:1174-1190)
-//   * PAPER.md kNN_S / data-parallel kNN          (PAPER.md:1206-1224, 1285-1287)
-//   * PAPER.md Alg. 3 Insert_L, Alg. 4 Erase_L   (PAPER.md:1229-1269, 721-730)
+//   * PAPER.md Alg. 1 BuildvEB_S                 (/root/reference/PAPER.md:1056-1093)
+//   * PAPER.md Alg. 2 Erase_S                    (PAPER.md:1121-1141)
+//   * PAPER.md kNN_S / data-parallel kNN          (PAPER.md:1153-1160, 1231-1233)
+//   * PAPER.md Alg. 3 Insert_L, Alg. 4 Erase_L   (PAPER.md:1178-1216, 721-730)
 //   * PAPER.md implementation details            (leaf 16, X=1024,
 //                                                  spatial median, largest->smallest trees)
 //   * SPEC.md kdtree / bdltree contracts
@@ -346,7 +346,7 @@ static void insert_range(const Tree& T, const double* q, std::uint32_t s, std::u
   }
 }
 
-// kNN_S (PAPER.md:1212-1213): descend to q's leaf, then while unwinding:
+// kNN_S (PAPER.md:1157-1160): descend to q's leaf, then while unwinding:
 // sibling-fill while the buffer holds fewer than k entries; otherwise
 // include-all / prune / recurse against the buffer's k-th bound (strict prune,
 // frozen decision 2).
@@ -390,7 +390,7 @@ static inline bool in_box(const double* p, const Node& nd, int d) {
   return true;
 }
 
-// Alg. 2 (PAPER.md:1181-1187): route the batch down by the children's boxes
+// Alg. 2 (PAPER.md:1126-1135): route the batch down by the children's boxes
 // (frozen decision 9), tombstone coordinate-exact matches in leaves, collapse
 // single-child nodes.  Returns the surviving slot or -1.
 static std::int32_t erase_rec(Tree& T, std::int32_t slot, const std::vector<const double*>& Q, std::size_t& killed) {
@@ -464,7 +464,7 @@ static void gather_live(const Tree& T, std::vector<double>& pts, std::vector<Id>
   }
 }
 
-// Insert_L (Alg. 3, PAPER.md:1233-1248; SPEC.md:572-580; frozen decisions 7-8).
+// Insert_L (Alg. 3, PAPER.md:1178-1195; SPEC.md:572-580; frozen decisions 7-8).
 static void insert_l(Bdl& b, const double* P, const Id* ids, std::size_t n) {
   const int d = b.d;
   const std::uint64_t X = b.X;
@@ -513,14 +513,14 @@ static void insert_l(Bdl& b, const double* P, const Id* ids, std::size_t n) {
   }
   b.F = Fn;
   if (b.statics.size() < 64) b.statics.resize(64);
-  for (std::size_t t = 0; t < order.size(); ++t) {  // builds of distinct new trees (PAPER.md:1193)
+  for (std::size_t t = 0; t < order.size(); ++t) {  // builds of distinct new trees (PAPER.md:1185)
     const int i = order[t];
     if (cnts[t] == 0) { b.F &= ~(1ULL << i); b.statics[i] = Tree(); continue; }
     build_tree(b.statics[i], d, pool_pts.data() + offs[t] * d, pool_ids.data() + offs[t], cnts[t], b.leaf, b.heuristic);
   }
 }
 
-// Erase_L (Alg. 4, PAPER.md:1259-1269; SPEC.md:581-589, 631).
+// Erase_L (Alg. 4, PAPER.md:1203-1216; SPEC.md:581-589, 631).
 static std::size_t erase_l(Bdl& b, const double* P, std::size_t n) {
   const int d = b.d;
   std::size_t killed = 0;
@@ -562,7 +562,7 @@ static std::size_t erase_l(Bdl& b, const double* P, std::size_t n) {
   return killed;
 }
 
-// kNN_L (PAPER.md:1285-1287, 1477-1479): one buffer per query; trees serially
+// kNN_L (PAPER.md:774-775, 1231-1233, 1477-1480): one buffer per query; trees serially
 // largest -> smallest, then the buffer tree; queries in parallel.
 static void knn_l(const Bdl& b, const double* Q, std::size_t nq, int k, Id* out_ids, double* out_d2,
                   KnnStats* stats) {

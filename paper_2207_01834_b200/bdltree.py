@@ -36,6 +36,10 @@ class GpuError(RuntimeError):
     pass
 
 
+class CapacityError(ValueError):
+    """range search: more rows than the caller's capacity (GK_ERR_CAPACITY); offsets were written"""
+
+
 class _Info(C.Structure):
     _fields_ = [("F", C.c_uint64), ("buffer", C.c_uint64), ("live", C.c_uint64), ("next_id", C.c_uint64),
                 ("build_size", C.c_uint64 * 64), ("live_per_tree", C.c_uint64 * 64),
@@ -126,6 +130,8 @@ def _check(rc: int) -> None:
         raise GpuError(msg)
     if rc == 3:
         raise NotImplementedError(msg)
+    if rc == 5:
+        raise CapacityError(msg)
     raise RuntimeError(msg)
 
 

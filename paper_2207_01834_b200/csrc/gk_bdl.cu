@@ -3,10 +3,10 @@
 //
 // Reference semantics (restated; the reference ships no code for it):
 //   BDLTree type        SPEC.md:549-555 (buffer tree, statics[i] of X*2^i, bitmask F)
-//   Insert_L (Alg. 3)   PAPER.md:1229-1248, 721-730; SPEC.md:572-580, 617-619
-//   Erase_L  (Alg. 4)   PAPER.md:1255-1269; SPEC.md:581-589, 631
-//   Erase_S  (Alg. 2)   PAPER.md:1174-1194; SPEC.md:479-487, 525
-//   kNN_L               PAPER.md:1285-1287, 1477-1479; SPEC.md:590-597
+//   Insert_L (Alg. 3)   PAPER.md:1178-1195, 721-730; SPEC.md:572-580, 617-619
+//   Erase_L  (Alg. 4)   PAPER.md:1203-1216; SPEC.md:581-589, 631
+//   Erase_S  (Alg. 2)   PAPER.md:1121-1141; SPEC.md:479-487, 525
+//   kNN_L               PAPER.md:774-775, 1231-1233, 1477-1480; SPEC.md:590-597
 // Frozen decisions (identical in oracle/gk_oracle.cpp):
 //   * ids are global insertion ordinals; Erase_L reinsertions keep their ids
 //   * Insert_L: the LAST |P| mod X points go to the buffer; on overflow the X
@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
         bool in = true;
 #pragma unroll
         for (int j = 0; j < D; ++j) in = in && (pf_hi[j] >= nd.lo[j][s]) && (pf_lo[j] <= nd.hi[j][s]);
-        if (in && sp < kStack) stk[sp++] = nd.ref[s];
+        if (in) {
+          if (sp >= kStack) __trap();  // unreachable: tree depth <= kDepthCap + 31 < kStack
+          stk[sp++] = nd.ref[s];
+        }
       }
     }
     if (local) atomicAdd(&killed[t], local);
@@ -427,7 +430,7 @@ struct gk_bdl {
     GK_CHECK_LAUNCH();
     tr("pool staged (launches)", static_cast<long long>(pool_n));
     // build the new trees, largest first, from contiguous pool slices; distinct trees
-    // build concurrently on their own streams (PAPER.md:1193)
+    // build concurrently on their own streams (PAPER.md:1185)
     F = Fn;
     std::vector<int> order;
     std::vector<std::uint64_t> offs, cnts;
@@ -653,6 +656,23 @@ struct DevScope {  // make the handle's GPU current for the call
     if (cur != prev) cudaSetDevice(prev);
   }
 };
+// frees the stream-ordered temporaries of a call on every exit path (no throw from the destructor)
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* take(std::size_t count) {
+    T* p = dalloc<T>(count, st);
+    ptrs.push_back(p);
+    return p;
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -1147,26 +1167,20 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
   const bool rows = offs_dev && (ids_dev || d2_dev);
   if (rows) need(ids_dev && d2_dev, "range rows need both ids and d2");
   const TreeSet ts = h->trees();
-  unsigned long long* cnt = counts_dev ? counts_dev : dalloc<unsigned long long>(nq + 1, h->st);
+  Scratch tmp(h->st);
+  unsigned long long* cnt = counts_dev ? counts_dev : tmp.take<unsigned long long>(nq + 1);
   GK_CUDA(cudaMemsetAsync(cnt, 0, (nq + (counts_dev ? 0 : 1)) * 8, h->st));
   std::uint32_t* perm = nullptr;
   std::uint32_t* ti = nullptr;
   double* td = nullptr;
   const bool slots = rows && nq * kRangeSlots * 12 <= kRangeSlotBytes;
   std::uint64_t total = 0;
-  auto release = [&] {
-    if (perm) dfree(perm, h->st);
-    if (ti) dfree(ti, h->st);
-    if (td) dfree(td, h->st);
-    if (!counts_dev) dfree(cnt, h->st);
-    GK_CUDA(cudaStreamSynchronize(h->st));
-  };
   if (ts.count > 0) {
-    perm = dalloc<std::uint32_t>(nq, h->st);
+    perm = tmp.take<std::uint32_t>(nq);
     range_order(h->d, q_dev, nq, perm, h->st);
     if (slots) {
-      ti = dalloc<std::uint32_t>(nq * kRangeSlots, h->st);
-      td = dalloc<double>(nq * kRangeSlots, h->st);
+      ti = tmp.take<std::uint32_t>(nq * kRangeSlots);
+      td = tmp.take<double>(nq * kRangeSlots);
       range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, cnt, nullptr, ti, td, 2, kRangeSlots, h->st);
     } else {
       range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, cnt, nullptr, nullptr, nullptr, 0, 0, h->st);
@@ -1175,27 +1189,24 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
   if (offs_dev) {
     std::size_t tb = 0;
     GK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs_dev, nq + 1, h->st));
-    void* tmp = dalloc<char>(tb, h->st);
-    GK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs_dev, nq + 1, h->st));
-    dfree(tmp, h->st);
+    GK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.take<char>(tb), tb, cnt, offs_dev, nq + 1, h->st));
     unsigned long long t = 0;
     GK_CUDA(cudaMemcpyAsync(&t, offs_dev + nq, 8, cudaMemcpyDeviceToHost, h->st));
     GK_CUDA(cudaStreamSynchronize(h->st));
     total = t;
     if (rows) {
-      if (total > capacity) {
-        release();
-        throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
-                                        std::to_string(capacity) + ")");
-      }
+      if (total > capacity)  // offsets are valid: the caller may size its buffers and call again
+        throw Error(GK_ERR_CAPACITY, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
+                                         std::to_string(capacity) + ")");
+      if (total > 0x7fffffffULL)  // the per-query row sort's limit, checked before any row is written
+        throw Error(GK_ERR_UNSUPPORTED, "range result larger than 2^31-1 rows");
       if (total > 0) {
         if (slots) {
-          std::uint32_t* ovf = dalloc<std::uint32_t>(nq, h->st);
+          std::uint32_t* ovf = tmp.take<std::uint32_t>(nq);
           const std::uint64_t no =
               range_slots_compact(nq, kRangeSlots, perm, cnt, offs_dev, ti, td, ids_dev, d2_dev, ovf, h->st);
           if (no)  // the overflowing queries again (in K2 order), rows straight to their offsets
             range_launch(h->d, ts, q_dev, no, r2, r2q_dev, ovf, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
-          dfree(ovf, h->st);
         } else {
           range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
         }
@@ -1203,7 +1214,7 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
       }
     }
   }
-  release();
+  GK_CUDA(cudaStreamSynchronize(h->st));
   return total;
 }
 
@@ -1211,6 +1222,7 @@ int gk_bdl_range_count(gk_bdl* h, const double* q, uint64_t nq, double r2, uint6
   return guard([&] {
     need(h != nullptr, "null handle");
     need(nq == 0 || (q && counts), "null buffer");
+    need(!std::isnan(r2) && r2 >= 0.0, "r2 must be a non-negative squared radius");
     DevScope ds(h->device);
     if (nq == 0) return;
     double* dq = dalloc<double>(nq * h->d, h->st);
@@ -1230,6 +1242,7 @@ int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* o
     need(h != nullptr, "null handle");
     need(offsets != nullptr && (nq == 0 || q), "null buffer");
     need(capacity == 0 || (ids && d2), "null row buffers");
+    need(!std::isnan(r2) && r2 >= 0.0, "r2 must be a non-negative squared radius");
     DevScope ds(h->device);
     if (nq == 0) {
       offsets[0] = 0;
@@ -1250,8 +1263,12 @@ int gk_bdl_range(gk_bdl* h, const double* q, uint64_t nq, double r2, uint64_t* o
     std::uint64_t total = 0;
     try {  // one count pass, one fill pass into the caller-sized row buffers
       total = range_device_impl(h, dq, nq, r2, nullptr, doff, di, dd, capacity);
+    } catch (const Error& e) {
+      if (e.code == GK_ERR_CAPACITY)  // offsets are final even when the rows do not fit
+        cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);
+      release();
+      throw;
     } catch (...) {
-      cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);  // offsets even when the rows do not fit
       release();
       throw;
     }
@@ -1334,8 +1351,12 @@ int gk_bdl_range_radii(gk_bdl* h, const double* q, uint64_t nq, const double* r2
     std::uint64_t total = 0;
     try {
       total = range_device_impl(h, dq, nq, 0.0, nullptr, doff, di, dd, capacity, dr);
+    } catch (const Error& e) {
+      if (e.code == GK_ERR_CAPACITY)  // offsets are final even when the rows do not fit
+        cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);
+      release();
+      throw;
     } catch (...) {
-      cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);  // offsets even when the rows do not fit
       release();
       throw;
     }
@@ -1413,7 +1434,7 @@ static std::uint64_t range_box_device_impl(gk_bdl* h, const double* lo, const do
   if (!counts_dev) dfree(cnt, h->st);
   GK_CUDA(cudaStreamSynchronize(h->st));
   if (too_small)
-    throw Error(GK_ERR_INVALID, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
+    throw Error(GK_ERR_CAPACITY, "range result (" + std::to_string(total) + " rows) exceeds the capacity (" +
                                     std::to_string(capacity) + ")");
   return total;
 }
@@ -1463,8 +1484,12 @@ int gk_bdl_range_box(gk_bdl* h, const double* lo, const double* hi, uint64_t nq,
     std::uint64_t total = 0;
     try {  // one count pass, one fill pass into the caller-sized row buffer
       total = range_box_device_impl(h, dl, dh, nq, nullptr, doff, di, capacity);
+    } catch (const Error& e) {
+      if (e.code == GK_ERR_CAPACITY)  // offsets are final even when the rows do not fit
+        cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);
+      release();
+      throw;
     } catch (...) {
-      cudaMemcpy(offsets, doff, (nq + 1) * 8, cudaMemcpyDeviceToHost);  // offsets even when the rows do not fit
       release();
       throw;
     }

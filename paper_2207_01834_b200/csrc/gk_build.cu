@@ -3,7 +3,7 @@
 // grid-wide barriers, so no level ever returns to the host.
 //
 // Reference semantics (restated; the reference ships no code for it):
-//   PAPER.md:1110-1127 Alg. 1 BuildvEB_S, 1141-1146 recursion, 1484-1487 spatial
+//   PAPER.md:1056-1093 Alg. 1 BuildvEB_S, 1110-1113 recursion, 1484-1487 spatial
 //   median = (min+max)/2, 1491 leaf 16.
 // Frozen decisions (mirrored by oracle/gk_oracle.cpp):
 //   split dim = depth mod D; spatial split s = (lo+hi)/2, left x_c < s <= right;
@@ -1074,11 +1074,12 @@ int coresident_blocks(const void* fn) {
 
 template <int D>
 int capacity_d() {
-  static int maxb = 0;  // per D
-  if (!maxb)
-    maxb = std::min(coresident_blocks(reinterpret_cast<const void*>(k_build<D, 0>)),
-                    coresident_blocks(reinterpret_cast<const void*>(k_build<D, 1>)));
-  return maxb;
+  static int maxb[kMaxDevices] = {};  // per D and device
+  const int dev = current_device();
+  if (!maxb[dev])
+    maxb[dev] = std::min(coresident_blocks(reinterpret_cast<const void*>(k_build<D, 0>)),
+                         coresident_blocks(reinterpret_cast<const void*>(k_build<D, 1>)));
+  return maxb[dev];
 }
 
 // grid of a build running alone: co-resident blocks, fewer for small trees (barriers are

@@ -31,6 +31,16 @@ struct Error : std::runtime_error {
 
 #define GK_CHECK_LAUNCH() GK_CUDA(cudaGetLastError())
 
+// Kernel attributes and occupancy-derived grid sizes are cached per (instantiation, device): a
+// process may drive handles on several GPUs, and the dynamic-shared-memory opt-in is per device.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  GK_CUDA(cudaGetDevice(&d));
+  if (d < 0 || d >= kMaxDevices) throw Error(GK_ERR_UNSUPPORTED, "device index >= 64");
+  return d;
+}
+
 // Traversal node (query-optimised mirror of one internal canonical node):
 // both children's boxes, rounded outward to fp32 (conservative, so pruning
 // stays exact), interleaved per dimension (lo[j] = {child0, child1}) so one
@@ -140,7 +150,7 @@ struct TreeSet {
 // buffer.  One build can be in flight per scratch: build_begin launches the
 // cooperative build kernel on `st` (asynchronously), build_finish waits for it,
 // sizes the node arrays and emits them.  Builds of distinct trees on distinct
-// (stream, scratch) pairs run concurrently (PAPER.md:1193 builds new trees in parallel).
+// (stream, scratch) pairs run concurrently (PAPER.md:1185 builds new trees in parallel).
 struct BuildScratch {
   void* base = nullptr;
   std::size_t size = 0;
@@ -170,7 +180,7 @@ inline void build_tree(BuildScratch& sc, int d, int leaf, int heuristic, const d
   build_finish(sc);
 }
 void free_tree(DevTree& t, cudaStream_t st);
-// Erase_S collapse: after tombstoning, drop emptied leaves
+// Erase_S collapse (Alg. 2): after tombstoning, drop emptied leaves
 // and splice out internal nodes left with one child; relinks the canonical
 // nodes and the traversal nodes and updates root_slot / root_ref.
 void collapse_tree(int d, DevTree& t, cudaStream_t st);

@@ -2,8 +2,8 @@
 // multi-tree traversal kernel (K1).
 //
 // Reference semantics (restated; no reference code exists for it):
-//   kNN_S  PAPER.md:1206-1224 (descend, sibling fill, bbox include/prune/recurse)
-//   kNN_L  PAPER.md:1285-1287, 1477-1479; SPEC.md:590-597 — one k-buffer per query
+//   kNN_S  PAPER.md:1153-1160 (descend, sibling fill, bbox include/prune/recurse)
+//   kNN_L  PAPER.md:774-775, 1231-1233, 1477-1480; SPEC.md:590-597 — one k-buffer per query
 //          reused across the trees, trees visited largest -> smallest, then the buffer tree
 //   KnnBuffer ordering: lexicographic (d2, id), knn_buffer.hpp:18-19, 36-38, 42-46
 // kNN is exact, so the result is a pure function of the live point set: the
@@ -540,16 +540,15 @@ void launch_k(const TreeSet& ts, const double* Q, const std::uint32_t* perm, std
   // per-lane top-K columns in shared memory (KT < 0: in a global scratch heap instead)
   const int smem = KT < 0 ? 0 : (KT > 0 ? KT : k) * kWarps * 32 * 12;
   const int smem_max = KT < 0 ? 0 : (KT > 0 ? KT : kMaxRuntimeK) * kWarps * 32 * 12;
-  static std::once_flag once;             // per (D, K) instantiation
-  static int sm_count = 0;
-  std::call_once(once, [&] {
+  static std::once_flag once[kMaxDevices];  // per (D, K) instantiation and device
+  static int sm_counts[kMaxDevices] = {};
+  const int dev = current_device();
+  std::call_once(once[dev], [&] {
     GK_CUDA(cudaFuncSetAttribute(k_knn<D, KT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     GK_CUDA(cudaFuncSetAttribute(k_knn<D, KT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-    int dev = 0, sms = 0;
-    GK_CUDA(cudaGetDevice(&dev));
-    GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    sm_count = sms;
+    GK_CUDA(cudaDeviceGetAttribute(&sm_counts[dev], cudaDevAttrMultiProcessorCount, dev));
   });
+  const int sm_count = sm_counts[dev];
   int per = 0;  // resident blocks at this launch's shared-memory size
   GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_knn<D, KT, false>, kWarps * 32, smem));
   const int resident = std::max(1, per) * sm_count;
@@ -788,11 +787,12 @@ template <int D>
 void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, const double* r2q, unsigned long long* counts,
              unsigned long long* offs, std::uint32_t* ids, double* d2, int mode, unsigned capq, std::uint32_t* perm,
              cudaStream_t st) {
-  static int grid = 0;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    int dev = 0, sms = 0, per0 = 0, per1 = 0, per2 = 0;
-    GK_CUDA(cudaGetDevice(&dev));
+  static int grids[kMaxDevices] = {};
+  static std::once_flag once[kMaxDevices];
+  const int dev = current_device();
+  int& grid = grids[dev];
+  std::call_once(once[dev], [&] {
+    int sms = 0, per0 = 0, per1 = 0, per2 = 0;
     GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k_range<D, 0>, 256, 0));
     GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_range<D, 1>, 256, 0));
@@ -950,11 +950,12 @@ __global__ void k_box_centre(const double* __restrict__ lo, const double* __rest
 template <int D>
 void range_box_d(const TreeSet& ts, const double* lo, const double* hi, std::uint64_t nq, unsigned long long* counts,
                  const unsigned long long* offs, std::uint32_t* ids, bool fill, const std::uint32_t* perm, cudaStream_t st) {
-  static int grid = 0;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    int dev = 0, sms = 0, per0 = 0, per1 = 0;
-    GK_CUDA(cudaGetDevice(&dev));
+  static int grids[kMaxDevices] = {};
+  static std::once_flag once[kMaxDevices];
+  const int dev = current_device();
+  int& grid = grids[dev];
+  std::call_once(once[dev], [&] {
+    int sms = 0, per0 = 0, per1 = 0;
     GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per0, k_range_box<D, false>, 256, 0));
     GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_range_box<D, true>, 256, 0));

@@ -133,7 +133,12 @@ def test_range_edges(gk, oracle):
     ids = np.zeros(4, np.uint32); d2 = np.zeros(4, np.float64)
     rc = lib.gk_bdl_range(g._h, Q.ctypes.data_as(C.c_void_p), len(Q), 0.05, offs.ctypes.data_as(C.c_void_p),
                           ids.ctypes.data_as(C.c_void_p), d2.ctypes.data_as(C.c_void_p), 4)
-    assert rc == 1 and int(offs[-1]) == int(o.range(Q, 0.05)[0][-1]) > 4
+    assert rc == 5 and int(offs[-1]) == int(o.range(Q, 0.05)[0][-1]) > 4  # GK_ERR_CAPACITY
+    # an invalid radius fails before anything is computed and leaves the offsets alone
+    offs[:] = 7
+    rc = lib.gk_bdl_range(g._h, Q.ctypes.data_as(C.c_void_p), len(Q), float("nan"), offs.ctypes.data_as(C.c_void_p),
+                          ids.ctypes.data_as(C.c_void_p), d2.ctypes.data_as(C.c_void_p), 4)
+    assert rc == 1 and (offs == 7).all()
 
 
 def test_range_device(gk, oracle):
