@@ -31,6 +31,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "gk_common.cuh"
@@ -64,7 +66,9 @@ namespace cg = cooperative_groups;
 namespace gk {
 namespace {
 
-constexpr std::uint8_t F_LEAF = 1, F_OBJECT = 2;
+// F_SMALL: a node of at most a.Tsmall points (more than a leaf) whose whole subtree the bottom phase
+// (k_subtree) builds inside one block; the level loop treats it like a leaf
+constexpr std::uint8_t F_LEAF = 1, F_OBJECT = 2, F_SMALL = 4;
 constexpr int kThreads = 256;
 constexpr int kSelCap = 4096;  // object nodes per radix-select batch
 constexpr int kMaxLevels = 256;
@@ -104,7 +108,13 @@ struct SelState {
 };
 
 // control words (device)
-enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_COUNT = 8 };
+enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_NSMALL = 5, C_SUBCTR = 6, C_WORK = 7, C_COUNT = 8 };
+constexpr int kSubLevels = 64;  // local levels of a bottom-phase subtree (<= kDepthCap + 12 + 1)
+constexpr int kVLevels = 160;
+// trees up to this size use the bottom phase by default (measured: C1's trees of <= 512K points build
+// faster with it; C2's 8.4M-point tree slower -- its level loop is bandwidth-bound, the bottom phase
+// issue-bound); GK_SMALL_MAX_N overrides
+constexpr std::uint64_t kSmallMaxN = 1ull << 20;   // absolute levels a merge spans (small roots at depths <= ~72, + kSubLevels)
 
 struct BuildArgs {
   int leaf, heuristic;
@@ -126,6 +136,23 @@ struct BuildArgs {
   std::uint32_t* hist;      // [kSelCap * 256]
   std::uint32_t* bsum;      // [gridDim]
   std::uint32_t* int_by_slot;  // [cap + 1]
+  // bottom phase (k_subtree + k_merge): subtrees of nodes with leaf < count <= Tsmall, one block each
+  std::uint32_t Tsmall;        // 0: off (object-median heuristic, leaf < 4, or a tree that fits no block)
+  std::uint32_t rmax;          // capacity of the small-root arrays
+  std::uint32_t* small_list;   // [rmax] level-array index of every small root (unordered)
+  std::uint32_t* sub_base;     // [rmax] first record of the subtree's node region
+  std::uint32_t* sub_cnt;      // [rmax * kSubLevels] nodes per local level (level 0 = the root)
+  std::uint32_t* sub_nlev;     // [rmax] local levels
+  std::uint32_t *s_start, *s_count, *s_child;  // sub-node records, [2n] (a region of 2 * count per subtree);
+                                               // s_child: an internal record's first child record
+  std::uint8_t* s_flags;
+  double *s_split, *s_lo, *s_hi;
+  std::uint32_t *marks, *mscan;  // [n + 1] small-root starts marked / scanned (roots in start order)
+  std::uint32_t* order;          // [rmax] small roots in start order
+  std::uint32_t* V;              // [vcap + 1] per (level, root) node counts, scanned in place
+  std::uint32_t vcap;
+  std::uint32_t* new_off;        // [kMaxLevels + 2] merged level offsets
+  NodeArrays na2;                // merged level arrays (copied back into na)
 };
 
 // ------------------------------------------------------------ block helpers --
@@ -209,6 +236,64 @@ __device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::ui
   scan_finish(in, out, n, bsum, sh, map);
 }
 
+// ---- vEB slots, top-down, over complete level arrays (lvl_off[0..H]).  Depth d is the cut depth of
+// exactly one frame (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
+// pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees left of v's, all
+// restricted to the frame's levels (range propagation).  Writes ctrl[C_H] / ctrl[C_N] and the
+// slot -> internal flags k_slot_rank scans into TNode indices.
+__device__ void veb_phase(cg::grid_group& grid, const BuildArgs& a, const NodeArrays& na, std::uint32_t* lvl_off, int H) {
+  const std::uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const std::uint32_t gthreads = gridDim.x * blockDim.x;
+  const std::uint32_t N = __ldcg(&lvl_off[H]);
+  if (gtid == 0) {
+    lvl_off[H + 1] = N;
+    a.ctrl[C_H] = static_cast<std::uint32_t>(H);
+    a.ctrl[C_N] = N;
+    na.pos[0] = 0;
+  }
+  sync_all(grid);
+  for (int d = 1; d < H; ++d) {
+    int d0 = 0, l = H;  // locate the frame whose cut is at depth d
+    while (true) {
+      const int lb = static_cast<int>(hyperceiling_u(static_cast<std::uint64_t>((l + 1) / 2)));
+      const int lt = l - lb;
+      if (d == d0 + lt) break;
+      if (d < d0 + lt) l = lt;
+      else { d0 += lt; l = lb; }
+    }
+    const std::uint32_t off = __ldcg(&lvl_off[d]), S = __ldcg(&lvl_off[d + 1]) - off;
+    for (std::uint32_t v = gtid; v < S; v += gthreads) {
+      const std::uint32_t g = off + v;
+      std::uint32_t r = g;
+      for (int e = d; e > d0; --e) r = __ldcg(&na.parent[r]);
+      auto child_idx = [&](std::uint32_t x, int e) -> std::uint32_t {
+        return (x < __ldcg(&lvl_off[e + 1])) ? __ldcg(&na.cbase[x]) : __ldcg(&lvl_off[e + 2]);
+      };
+      std::uint32_t lo = r, hi = r + 1, top = 0;
+      for (int e = d0; e < d; ++e) {
+        top += hi - lo;
+        lo = child_idx(lo, e);
+        hi = child_idx(hi, e);
+      }
+      std::uint32_t x = g, y = lo, left = 0;
+      for (int e = d; e < d0 + l; ++e) {
+        left += x - y;
+        if (e + 1 < d0 + l) {
+          x = child_idx(x, e);
+          y = child_idx(y, e);
+        }
+      }
+      na.pos[g] = __ldcg(&na.pos[r]) + top + left;
+    }
+    sync_all(grid);
+  }
+  // slot -> internal flag (scanned into internal ranks = TNode indices by k_slot_rank)
+  for (std::uint32_t g = gtid; g <= N; g += gthreads) {
+    if (g == N) a.int_by_slot[N] = 0;
+    else a.int_by_slot[__ldcg(&na.pos[g])] = (__ldcg(&na.flags[g]) & F_LEAF) ? 0u : 1u;
+  }
+}
+
 // -------------------------------------------------------------- the build --
 #ifndef GK_BUILD_MINB
 #define GK_BUILD_MINB 4  // D <= 4: 64 registers, 4 blocks per SM (C2 build -4 % vs 80 registers)
@@ -271,6 +356,9 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     a.chunk_cnt[0] = (n + kc - 1) / kc;  // deeper levels' chunk counts are written by F
     a.chunk_cnt[1] = 0;
     a.ctrl[C_LEVEL] = 0xffffffffu;
+    a.ctrl[C_NSMALL] = 0;
+    a.ctrl[C_SUBCTR] = 0;
+    a.ctrl[C_WORK] = 0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       a.keys[j * 2] = ~0ULL;
@@ -331,8 +419,12 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
           na.hi[static_cast<std::uint64_t>(g) * D + j] = hi[j];
         }
         na.level[g] = static_cast<std::uint8_t>(level);
-        if (__ldcg(&na.count[g]) <= static_cast<std::uint32_t>(a.leaf)) {
+        const std::uint32_t cnt_g = __ldcg(&na.count[g]);
+        if (cnt_g <= static_cast<std::uint32_t>(a.leaf)) {
           na.flags[g] = F_LEAF;
+          na.split[g] = 0.0;
+        } else if (cnt_g <= a.Tsmall) {
+          na.flags[g] = F_SMALL;
           na.split[g] = 0.0;
         } else if (!spatial_level) {
           na.flags[g] = F_OBJECT;
@@ -404,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
         const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
         const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
         std::uint32_t cnt = 0;
-        if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf)) {
+        if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf) && nn > a.Tsmall) {
           const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
           const std::uint32_t end = min(first + kc, s0 + nn);
           const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
@@ -422,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
       std::uint32_t cnt = 0;
-      if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf)) {
+      if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf) && nn > a.Tsmall) {
         const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
         const std::uint32_t end = min(first + kc, s0 + nn);
         const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
@@ -465,7 +557,11 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       }
       const std::uint32_t g = off + v;
       std::uint8_t fl = __ldcg(&na.flags[g]);
-      if (fl & F_LEAF) { a.is_int[v] = 0; continue; }
+      if (fl & (F_LEAF | F_SMALL)) {
+        a.is_int[v] = 0;
+        if (fl & F_SMALL) a.small_list[atomicAdd(&a.ctrl[C_NSMALL], 1u)] = g;  // the bottom phase builds it
+        continue;
+      }
       a.is_int[v] = 1;
       const std::uint32_t cnt = __ldcg(&na.count[g]);
       if (!(fl & F_OBJECT)) {
@@ -595,7 +691,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const std::uint32_t g = off + v;
       const std::uint32_t cb = next_off + 2 * __ldcg(&a.irank[v]);
       na.cbase[g] = cb;
-      if (__ldcg(&na.flags[g]) & F_LEAF) continue;
+      if (__ldcg(&na.flags[g]) & (F_LEAF | F_SMALL)) continue;
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]), nl = __ldcg(&na.nleft[g]);
       na.start[cb] = s0; na.count[cb] = nl; na.parent[cb] = g;
       na.start[cb + 1] = s0 + nl; na.count[cb + 1] = nn - nl; na.parent[cb + 1] = g;
@@ -633,8 +729,8 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
           first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
           end = min(first + kc, s0 + nn);
         }
-        const bool part = !(fl & F_LEAF);
-        if (!part) {  // finished leaf (or no chunk): positions are final
+        const bool part = !(fl & (F_LEAF | F_SMALL));
+        if (!part) {  // finished leaf or small subtree root (or no chunk): positions are final for this loop
           for (std::uint32_t i = first + gla; i < end; i += gl) {
 #pragma unroll
             for (int j = 0; j < D; ++j) a.out[j * static_cast<std::uint64_t>(n) + i] = __ldcg(&cur[j * cur_stride + i]);
@@ -723,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
       const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
       const std::uint32_t end = min(first + kc, s0 + nn);
-      if (fl & F_LEAF) {  // finished: positions are final
+      if (fl & (F_LEAF | F_SMALL)) {  // finished (a small root's subtree is built by the bottom phase)
         for (std::uint32_t i = first + lane; i < end; i += 32) {
 #pragma unroll
           for (int j = 0; j < D; ++j) a.out[j * static_cast<std::uint64_t>(n) + i] = __ldcg(&cur[j * cur_stride + i]);
@@ -829,65 +925,541 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
   unsigned long long tv_a = 0, tv_b = 0;
   if (gtid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv_a));
 #endif
-  // ---- vEB slots, top-down.  Depth d is the cut depth of exactly one frame
-  // (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
-  // pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees
-  // left of v's, all restricted to the frame's levels (range propagation).
-  const int H = level;
-  const std::uint32_t N = __ldcg(&a.lvl_off[H]);
-  if (gtid == 0) {
-    a.lvl_off[H + 1] = N;
-    a.ctrl[C_H] = static_cast<std::uint32_t>(H);
-    a.ctrl[C_N] = N;
-    na.pos[0] = 0;
+  if (__ldcg(&a.ctrl[C_NSMALL]) > 0) {  // small subtrees pending: k_subtree + k_merge finish the tree
+    if (gtid == 0) a.ctrl[C_H] = static_cast<std::uint32_t>(level);  // the level loop's levels
+    GK_TL_PRINT(level0);
+    return;
   }
-  sync_all(grid);
-  for (int d = 1; d < H; ++d) {
-    int d0 = 0, l = H;  // locate the frame whose cut is at depth d
-    while (true) {
-      const int lb = static_cast<int>(hyperceiling_u(static_cast<std::uint64_t>((l + 1) / 2)));
-      const int lt = l - lb;
-      if (d == d0 + lt) break;
-      if (d < d0 + lt) l = lt;
-      else { d0 += lt; l = lb; }
-    }
-    const std::uint32_t off = __ldcg(&a.lvl_off[d]), S = __ldcg(&a.lvl_off[d + 1]) - off;
-    for (std::uint32_t v = gtid; v < S; v += gthreads) {
-      const std::uint32_t g = off + v;
-      std::uint32_t r = g;
-      for (int e = d; e > d0; --e) r = __ldcg(&na.parent[r]);
-      auto child_idx = [&](std::uint32_t x, int e) -> std::uint32_t {
-        return (x < __ldcg(&a.lvl_off[e + 1])) ? __ldcg(&na.cbase[x]) : __ldcg(&a.lvl_off[e + 2]);
-      };
-      std::uint32_t lo = r, hi = r + 1, top = 0;
-      for (int e = d0; e < d; ++e) {
-        top += hi - lo;
-        lo = child_idx(lo, e);
-        hi = child_idx(hi, e);
-      }
-      std::uint32_t x = g, y = lo, left = 0;
-      for (int e = d; e < d0 + l; ++e) {
-        left += x - y;
-        if (e + 1 < d0 + l) {
-          x = child_idx(x, e);
-          y = child_idx(y, e);
-        }
-      }
-      na.pos[g] = __ldcg(&na.pos[r]) + top + left;
-    }
-    sync_all(grid);
-  }
-  // slot -> internal flag (scanned into internal ranks = TNode indices by k_slot_rank)
-  for (std::uint32_t g = gtid; g <= N; g += gthreads) {
-    if (g == N) a.int_by_slot[N] = 0;
-    else a.int_by_slot[__ldcg(&na.pos[g])] = (__ldcg(&na.flags[g]) & F_LEAF) ? 0u : 1u;
-  }
+  veb_phase(grid, a, na, a.lvl_off, level);
 #if GK_BUILD_TIMELINE
   if (gtid == 0) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv_b));
-    printf("[tlveb] n=%u grid=%u H=%d N=%u vEB %.1f us\n", n, gridDim.x, H, N, (tv_b - tv_a) * 1e-3);
+    printf("[tlveb] n=%u grid=%u H=%d N=%u vEB %.1f us\n", n, gridDim.x, level, a.ctrl[C_N], (tv_b - tv_a) * 1e-3);
   }
 #endif
+}
+
+// ============================================================ bottom phase --
+// Nodes of at most a.Tsmall points (F_SMALL, registered by phase E of the level loop) have their
+// whole subtree built by k_subtree, one block per subtree, entirely in shared memory: the points are
+// read once and written once, and the subtree's levels cost block barriers instead of grid barriers
+// (the sparse bottom levels of the level loop were bound by per-chunk metadata latency).  Same split
+// rules as the level loop and the oracle (Alg. 1; frozen decisions 3-6): split
+// dim = depth mod D, spatial s = (lo + hi) / 2 with left x_c < s, degenerate side / depth >= 40 ->
+// object median by (x_c, id) with left = the floor(n/2) smallest keys, stable partitions.  k_merge
+// then interleaves the subtrees' nodes with the level loop's into complete level arrays (left-to-right
+// = start order at every level) and runs the vEB slot phase over them.
+constexpr int kSubThreads = 256;
+constexpr std::uint16_t kNoSeg = 0xffff;  // position of a leaf finished at an earlier level
+#ifdef GK_DBG
+#include <cassert>
+#define GK_ASSERT(c) assert(c)
+#else
+#define GK_ASSERT(c) do {} while (0)
+#endif
+#ifndef GK_SMALL_T
+#define GK_SMALL_T 1024
+#endif
+template <int D>
+__host__ __device__ constexpr int small_cap() {
+  return D <= 3 ? GK_SMALL_T : (D <= 5 ? GK_SMALL_T / 2 : GK_SMALL_T / 4);
+}
+template <int D>
+__host__ __device__ constexpr int small_nmax() {  // nodes per level of a subtree (leaf >= 4: internal nodes >= 5 points)
+  return 2 * small_cap<D>() / 5 + 2;
+}
+template <int D>
+__host__ __device__ constexpr std::size_t small_smem() {
+  constexpr int T = small_cap<D>(), NM = small_nmax<D>();
+  return static_cast<std::size_t>(T) * D * 8 + static_cast<std::size_t>(NM) * D * 16 + NM * 8 + T * 4 + NM * 4 +
+         NM * 4 + 32 * 4 + 16 + 2 * (kSubLevels + 1) * 4 + T * 2 * 4 + (T + 1) * 2 + NM * 2 * 4 + (NM + 1) * 2 + NM + 64;
+}
+
+// in-place exclusive scan of a[0, n) (a[n] = total) by the whole block; wsum: 32 words of shared memory
+__device__ void block_exscan_u16(std::uint16_t* a, int n, std::uint32_t* wsum) {
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  const int per = (n + nth - 1) / nth;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  std::uint32_t s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  std::uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    std::uint32_t v = lane < nw ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < nw) wsum[lane] = v;
+  }
+  __syncthreads();
+  std::uint32_t base = (wid ? wsum[wid - 1] : 0u) + x - s;
+  for (int i = lo; i < hi; ++i) {
+    const std::uint32_t t = a[i];
+    a[i] = static_cast<std::uint16_t>(base);
+    base += t;
+  }
+  if (tid == 0) a[n] = static_cast<std::uint16_t>(wsum[nw - 1]);
+  __syncthreads();
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
+  constexpr int T = small_cap<D>(), NM = small_nmax<D>();
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* X = reinterpret_cast<double*>(smem);                                     // [D][T]
+  unsigned long long* nbox = reinterpret_cast<unsigned long long*>(X + D * T);      // [NM][D][2] dkey
+  double* nsplit = reinterpret_cast<double*>(nbox + NM * D * 2);                    // [NM]
+  std::uint32_t* ID = reinterpret_cast<std::uint32_t*>(nsplit + NM);                // [T]
+  std::uint32_t* nthr = ID + T;                                                     // [NM]
+  std::uint32_t* nleft = nthr + NM;                                                 // [NM]
+  std::uint32_t* wsum = nleft + NM;                                                 // [32]
+  std::uint32_t* misc = wsum + 32;                                                  // [4]
+  std::uint32_t* lvo = misc + 4;                     // [kSubLevels + 1] region offset of each local level
+  std::uint32_t* lvc = lvo + kSubLevels + 1;         // [kSubLevels + 1] nodes of each local level
+  std::uint16_t* permA = reinterpret_cast<std::uint16_t*>(lvc + kSubLevels + 1);    // [T]
+  std::uint16_t* permB = permA + T;                                                 // [T]
+  std::uint16_t* seg = permB + T;                                                   // [T] position -> node
+  std::uint16_t* seg2 = seg + T;                                                    // [T] (next level)
+  std::uint16_t* Lsc = seg2 + T;                                                    // [T + 1]
+  std::uint16_t* nst = Lsc + T + 1;                                                 // [2][NM]
+  std::uint16_t* ncn = nst + 2 * NM;                                                // [2][NM]
+  std::uint16_t* nscan = ncn + 2 * NM;                                              // [NM + 1]
+  std::uint8_t* nfl = reinterpret_cast<std::uint8_t*>(nscan + NM + 1);              // [NM]
+
+  const NodeArrays& na = a.na;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const std::uint64_t N = a.n;  // SoA stride of the output
+  const bool spatial_heur = a.heuristic != GK_OBJECT_MEDIAN;
+  while (true) {
+    if (tid == 0) misc[0] = atomicAdd(&a.ctrl[C_WORK], 1u);
+    __syncthreads();
+    const std::uint32_t r = misc[0];
+    if (r >= __ldcg(&a.ctrl[C_NSMALL])) return;
+    const std::uint32_t g = __ldcg(&a.small_list[r]);
+    const std::uint32_t s0 = __ldcg(&na.start[g]);
+    const int n = static_cast<int>(__ldcg(&na.count[g]));
+    const int L = __ldcg(&na.level[g]);
+    if (tid == 0) misc[1] = atomicAdd(&a.ctrl[C_SUBCTR], 2u * static_cast<std::uint32_t>(n));
+    for (int i = tid; i < n; i += nth) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) X[j * T + i] = __ldcg(&a.out[j * N + s0 + i]);
+      ID[i] = __ldcg(&a.out_ids[s0 + i]);
+      permA[i] = static_cast<std::uint16_t>(i);
+      seg[i] = 0;
+    }
+    if (tid == 0) {
+      nst[0] = 0;
+      ncn[0] = static_cast<std::uint16_t>(n);
+    }
+    __syncthreads();
+    const std::uint32_t base = misc[1];
+    GK_ASSERT(base + 2u * n <= 2u * a.n && n <= T && r < a.rmax);
+    std::uint32_t rec = base;  // next record of the subtree's region (local levels >= 1, level-major)
+    std::uint16_t* perm = permA;
+    std::uint16_t* perm2 = permB;
+    int cb = 0, nc = 1, lv = 0;
+    for (;; ++lv) {
+      if (lv >= kSubLevels) __trap();  // unreachable: depth cap 40 + log2(T) + 1 levels
+      const int depth = L + lv, c = depth % D;
+      const bool spatial = spatial_heur && depth < kDepthCap;
+      std::uint16_t* cst = nst + cb * NM;
+      std::uint16_t* ccn = ncn + cb * NM;
+      // (a) node boxes.  A node's positions are contiguous: a segmented min/max scan inside each warp
+      // (shuffles between lanes of the same node), then one shared-memory atomic per node run per warp.
+      // Internal nodes need only the split dimension here (their full boxes are the unions of their
+      // children's, computed bottom-up after the last level); leaves need every dimension.
+      for (int i = tid; i < nc * D; i += nth) {
+        nbox[2 * i] = ~0ULL;
+        nbox[2 * i + 1] = 0ULL;
+      }
+      __syncthreads();
+      for (int p0 = wid * 32; p0 < n; p0 += nth) {
+        const int p = p0 + lane;
+        const int sg = p < n ? seg[p] : kNoSeg;
+        const bool valid = sg != kNoSeg;
+        if (!__any_sync(0xffffffffu, valid)) continue;  // only finished leaves in this chunk
+        const int node = valid ? sg : -1 - lane;        // invalid lanes: singleton runs
+        const bool isleaf = valid && ccn[sg] <= a.leaf;
+        const bool anyleaf = __any_sync(0xffffffffu, isleaf);
+        const int ip = valid ? perm[p] : 0;
+        unsigned same = 0;  // bit o: the lane 2^o below belongs to the same node
+#pragma unroll
+        for (int o = 0; o < 5; ++o) {
+          const int up = __shfl_up_sync(0xffffffffu, node, 1 << o);
+          if (lane >= (1 << o) && up == node) same |= 1u << o;
+        }
+        const int dn = __shfl_down_sync(0xffffffffu, node, 1);
+        const bool tail = valid && (lane == 31 || dn != node);
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          if (j != c && !anyleaf) continue;  // warp-uniform
+          const bool use = valid && (j == c || isleaf);
+          unsigned long long mn = use ? dkey(X[j * T + ip]) : ~0ULL, mx = use ? mn : 0ULL;
+#pragma unroll
+          for (int o = 0; o < 5; ++o) {
+            const unsigned long long a1 = __shfl_up_sync(0xffffffffu, mn, 1 << o);
+            const unsigned long long b1 = __shfl_up_sync(0xffffffffu, mx, 1 << o);
+            if (same >> o & 1u) {
+              mn = a1 < mn ? a1 : mn;
+              mx = b1 > mx ? b1 : mx;
+            }
+          }
+          if (tail && use) {
+            atomicMin(&nbox[(node * D + j) * 2], mn);
+            atomicMax(&nbox[(node * D + j) * 2 + 1], mx);
+          }
+        }
+      }
+      __syncthreads();
+      // (b) leaf / spatial split / object
+      for (int i = tid; i < nc; i += nth) {
+        const int cnt = ccn[i];
+        std::uint8_t fl = 0;
+        if (cnt <= a.leaf) {
+          fl = F_LEAF;
+          nsplit[i] = 0.0;
+        } else if (spatial) {
+          const double l = dkey_inv(nbox[(i * D + c) * 2]), h = dkey_inv(nbox[(i * D + c) * 2 + 1]);
+          nsplit[i] = __dmul_rn(__dadd_rn(l, h), 0.5);  // (lo + hi) / 2 exactly
+        } else {
+          fl = F_OBJECT;
+        }
+        nfl[i] = fl;
+        nleft[i] = 0;
+        nthr[i] = 0;
+        nscan[i] = (fl & F_LEAF) ? 0 : 1;  // internal nodes -> child slots of the next level
+      }
+      __syncthreads();
+      block_exscan_u16(nscan, nc, wsum);
+      const int nint = nscan[nc];
+      // (c) spatial left counts (warp-aggregated per node)
+      for (int p0 = wid * 32; p0 < n; p0 += nth) {
+        const int p = p0 + lane;
+        const int sg = p < n ? seg[p] : kNoSeg;
+        const bool valid = sg != kNoSeg;
+        const int node = valid ? sg : -1;
+        bool pr = false;
+        if (valid && nfl[node] == 0) pr = X[c * T + perm[p]] < nsplit[node];
+        const unsigned grp = __match_any_sync(0xffffffffu, node);
+        const unsigned pm = __ballot_sync(0xffffffffu, pr);
+        if (valid && nfl[node] == 0 && lane == __ffs(grp) - 1 && (pm & grp)) atomicAdd(&nleft[node], __popc(pm & grp));
+      }
+      __syncthreads();
+      // (d) degenerate spatial splits -> object median; object nodes keep the floor(n/2) smallest keys
+      for (int i = tid; i < nc; i += nth) {
+        const std::uint32_t cnt = ccn[i];
+        std::uint8_t fl = nfl[i];
+        if (fl == 0 && (nleft[i] == 0 || nleft[i] == cnt)) fl = F_OBJECT;
+        if (fl == F_OBJECT) nleft[i] = cnt / 2;
+        nfl[i] = fl;
+      }
+      __syncthreads();
+      // (e) object thresholds: the key of rank floor(n/2) in (x_c, id) order (-0 == +0), by rank counting
+      for (int p = tid; p < n; p += nth) {
+        const int node = seg[p];
+        if (node == kNoSeg || nfl[node] != F_OBJECT) continue;
+        const int ip = perm[p];
+        const double xp = X[c * T + ip];
+        const std::uint32_t idp = ID[ip];
+        const int st = cst[node], cn = ccn[node];
+        std::uint32_t rank = 0;
+        for (int q = st; q < st + cn; ++q) {
+          const int iq = perm[q];
+          const double xq = X[c * T + iq];
+          rank += (xq < xp || (xq == xp && ID[iq] < idp)) ? 1u : 0u;
+        }
+        if (rank == nleft[node]) {  // keys are unique (ids are): exactly one position writes
+          nsplit[node] = __dadd_rn(xp, 0.0);  // canonical +0 for a zero median, as the level loop
+          nthr[node] = idp;
+        }
+      }
+      __syncthreads();
+      // (f) partition predicate, block scan
+      for (int p = tid; p < n; p += nth) {
+        const int node = seg[p];
+        const std::uint8_t fl = node == kNoSeg ? F_LEAF : nfl[node];
+        bool pr = false;
+        if (!(fl & F_LEAF)) {
+          const int ip = perm[p];
+          const double x = X[c * T + ip];
+          const double sp = nsplit[node];
+          pr = (fl & F_OBJECT) ? (x < sp || (x == sp && ID[ip] < nthr[node])) : (x < sp);
+        }
+        Lsc[p] = pr ? 1 : 0;
+      }
+      __syncthreads();
+      block_exscan_u16(Lsc, n, wsum);
+      // (g) stable partition of the positions (leaves keep theirs); the next level's position -> node map
+      for (int p = tid; p < n; p += nth) {
+        const int node = seg[p];
+        int np = p;
+        std::uint16_t child = kNoSeg;
+        if (node != kNoSeg && !(nfl[node] & F_LEAF)) {
+          const int st = cst[node];
+          const int lr = Lsc[p] - Lsc[st];
+          const bool pr = Lsc[p + 1] != Lsc[p];
+          np = pr ? st + lr : st + static_cast<int>(nleft[node]) + (p - st - lr);
+          child = static_cast<std::uint16_t>(2 * nscan[node] + (pr ? 0 : 1));
+        }
+        perm2[np] = perm[p];
+        seg2[np] = child;
+      }
+      // (h) this level's node records; internal nodes -> the next level's nodes
+      std::uint16_t* xst = nst + (cb ^ 1) * NM;
+      std::uint16_t* xcn = ncn + (cb ^ 1) * NM;
+      for (int i = tid; i < nc; i += nth) {
+        const std::uint8_t fl = nfl[i];
+        const int st = cst[i], cnt = ccn[i];
+        if (!(fl & F_LEAF)) {
+          const int k2 = 2 * nscan[i];
+          xst[k2] = static_cast<std::uint16_t>(st);
+          xcn[k2] = static_cast<std::uint16_t>(nleft[i]);
+          xst[k2 + 1] = static_cast<std::uint16_t>(st + nleft[i]);
+          xcn[k2 + 1] = static_cast<std::uint16_t>(cnt - static_cast<int>(nleft[i]));
+        }
+        if (lv == 0) {  // the subtree root is the level loop's node g: finish its record
+          na.flags[g] = fl;
+          na.split[g] = nsplit[i];
+          na.thr_id[g] = nthr[i];
+        } else {
+          const std::uint32_t ri = rec + i;
+          GK_ASSERT(ri < base + 2u * n);
+          a.s_start[ri] = s0 + st;
+          a.s_count[ri] = cnt;
+          a.s_flags[ri] = fl;
+          a.s_split[ri] = nsplit[i];
+          if (fl & F_LEAF) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              a.s_lo[static_cast<std::uint64_t>(ri) * D + j] = dkey_inv(nbox[(i * D + j) * 2]);
+              a.s_hi[static_cast<std::uint64_t>(ri) * D + j] = dkey_inv(nbox[(i * D + j) * 2 + 1]);
+            }
+          } else {
+            a.s_child[ri] = rec + nc + 2u * nscan[i];  // the next level's records follow this level's
+          }
+        }
+      }
+      if (tid == 0) {
+        a.sub_cnt[static_cast<std::uint64_t>(r) * kSubLevels + lv] = static_cast<std::uint32_t>(nc);
+        lvo[lv] = rec;
+        lvc[lv] = static_cast<std::uint32_t>(nc);
+      }
+      if (lv > 0) rec += nc;
+      __syncthreads();
+      {
+        std::uint16_t* t = perm;
+        perm = perm2;
+        perm2 = t;
+      }
+      if (nint == 0) break;
+      cb ^= 1;
+      nc = 2 * nint;
+      if (nc > NM) __trap();  // unreachable for leaf >= 4
+      {
+        std::uint16_t* t = seg;
+        seg = seg2;
+        seg2 = t;
+      }
+    }
+    // internal nodes' boxes, bottom-up: the union of their children's (dkey order, as the level loop's
+    // atomics; the root's box came from the level loop)
+    for (int l2 = lv - 1; l2 >= 1; --l2) {
+      const std::uint32_t r0 = lvo[l2], rc = lvc[l2];
+      for (std::uint32_t i = tid; i < rc; i += nth) {
+        const std::uint32_t ri = r0 + i;
+        if (a.s_flags[ri] & F_LEAF) continue;
+        const std::uint64_t c0 = a.s_child[ri];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double l0 = a.s_lo[c0 * D + j], l1 = a.s_lo[(c0 + 1) * D + j];
+          const double h0 = a.s_hi[c0 * D + j], h1 = a.s_hi[(c0 + 1) * D + j];
+          a.s_lo[static_cast<std::uint64_t>(ri) * D + j] = dkey(l1) < dkey(l0) ? l1 : l0;
+          a.s_hi[static_cast<std::uint64_t>(ri) * D + j] = dkey(h1) > dkey(h0) ? h1 : h0;
+        }
+      }
+      __syncthreads();
+    }
+    // the subtree's points in their final (leaf) order
+    for (int p = tid; p < n; p += nth) {
+      const int ip = perm[p];
+#pragma unroll
+      for (int j = 0; j < D; ++j) a.out[j * N + s0 + p] = X[j * T + ip];
+      a.out_ids[s0 + p] = ID[ip];
+    }
+    if (tid == 0) {
+      a.sub_base[r] = base;
+      a.sub_nlev[r] = static_cast<std::uint32_t>(lv + 1);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ std::uint32_t lower_bound_u32(const std::uint32_t* a, std::uint32_t lo, std::uint32_t hi,
+                                                         std::uint32_t x) {  // first i in [lo, hi) with a[i] >= x
+  while (lo < hi) {
+    const std::uint32_t mid = (lo + hi) >> 1;
+    if (__ldcg(&a[mid]) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Interleaves the subtrees' nodes with the level loop's ones.  At every level the left-to-right order
+// is the order of the nodes' first points (disjoint ranges), so: small roots in start order, per
+// (level, root) node counts scanned into positions, each node's merged index = level offset +
+// (level-loop nodes left of it) + (subtree nodes left of it), then parent and first-child indices by
+// binary search over each level's starts, then the vEB phase.  The merged arrays are a.na2 (parent,
+// cbase and pos shared with a.na); k_emit reads a.na2 when the bottom phase ran.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ std::uint32_t sh[32];
+  const NodeArrays& na = a.na;
+  const NodeArrays& nb = a.na2;
+  const std::uint32_t R = __ldcg(&a.ctrl[C_NSMALL]);
+  if (R == 0) return;
+  const std::uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, gthreads = gridDim.x * blockDim.x;
+  const std::uint32_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+  const int lane = threadIdx.x & 31;
+  const std::uint32_t n = a.n;
+  const int HA = static_cast<int>(__ldcg(&a.ctrl[C_H]));  // level-loop levels
+  const std::uint32_t NA = __ldcg(&a.lvl_off[HA]);
+  // small roots' first points marked over the points and scanned: rank(x) = # roots starting before x
+  for (std::uint32_t i = gtid; i <= n; i += gthreads) a.marks[i] = 0;
+  if (gtid == 0) {
+    a.ctrl[C_S] = static_cast<std::uint32_t>(HA);  // max level + 1
+    a.ctrl[C_NOBJ] = 0xffffffffu;                  // min root level
+  }
+  sync_all(grid);
+  for (std::uint32_t r = gtid; r < R; r += gthreads) {
+    const std::uint32_t g = __ldcg(&a.small_list[r]);
+    a.marks[__ldcg(&na.start[g])] = 1;
+    const std::uint32_t L = __ldcg(&na.level[g]);
+    atomicMax(&a.ctrl[C_S], L + __ldcg(&a.sub_nlev[r]));
+    atomicMin(&a.ctrl[C_NOBJ], L);
+  }
+  sync_all(grid);
+  grid_scan(grid, a.marks, a.mscan, n + 1, a.bsum, sh);
+  sync_all(grid);
+  const int H = static_cast<int>(__ldcg(&a.ctrl[C_S]));
+  const int Lmin = static_cast<int>(__ldcg(&a.ctrl[C_NOBJ]));
+  // # small roots whose first point precedes position x
+  auto root_rank = [&](std::uint32_t x) -> std::uint32_t { return __ldcg(&a.mscan[x]); };
+  for (std::uint32_t r = gtid; r < R; r += gthreads) {
+    const std::uint32_t k = root_rank(__ldcg(&na.start[__ldcg(&a.small_list[r])]));
+    GK_ASSERT(k < R);
+    a.order[k] = r;
+  }
+  const std::uint32_t span = static_cast<std::uint32_t>(H - Lmin - 1);  // levels Lmin + 1 .. H - 1 hold subtree nodes
+  if (static_cast<std::uint64_t>(span) * R + 1 > a.vcap) __trap();       // unreachable: vcap = rmax x 160 levels
+  sync_all(grid);
+  // V[(l - Lmin - 1) * R + k] = nodes of root order[k] at level l, scanned in place
+  const std::uint32_t VN = span * R;
+  for (std::uint32_t i = gtid; i <= VN; i += gthreads) {
+    std::uint32_t v = 0;
+    if (i < VN) {
+      const int l = Lmin + 1 + static_cast<int>(i / R);
+      const std::uint32_t r = __ldcg(&a.order[i % R]);
+      const int lam = l - static_cast<int>(__ldcg(&na.level[__ldcg(&a.small_list[r])]));
+      if (lam >= 1 && lam < static_cast<int>(__ldcg(&a.sub_nlev[r])))
+        v = __ldcg(&a.sub_cnt[static_cast<std::uint64_t>(r) * kSubLevels + lam]);
+    }
+    a.V[i] = v;
+  }
+  sync_all(grid);
+  grid_scan(grid, a.V, a.V, VN + 1, a.bsum, sh);
+  sync_all(grid);
+  if (gtid == 0) {
+    std::uint32_t acc = 0;
+    for (int l = 0; l < H; ++l) {
+      a.new_off[l] = acc;
+      const std::uint32_t A = l < HA ? __ldcg(&a.lvl_off[l + 1]) - __ldcg(&a.lvl_off[l]) : 0u;
+      std::uint32_t S = 0;
+      if (l > Lmin) S = __ldcg(&a.V[(l - Lmin) * R]) - __ldcg(&a.V[(l - Lmin - 1) * R]);
+      acc += A + S;
+    }
+    a.new_off[H] = acc;
+    a.new_off[H + 1] = acc;
+  }
+  sync_all(grid);
+  // scatter the level loop's nodes
+  for (std::uint32_t x = gtid; x < NA; x += gthreads) {
+    const int l = __ldcg(&na.level[x]);
+    const std::uint32_t st = __ldcg(&na.start[x]);
+    std::uint32_t y = __ldcg(&a.new_off[l]) + (x - __ldcg(&a.lvl_off[l]));
+    if (l > Lmin) {
+      const std::uint32_t row = (l - Lmin - 1) * R;
+      y += __ldcg(&a.V[row + root_rank(st)]) - __ldcg(&a.V[row]);
+    }
+    GK_ASSERT(y < 2 * n - 1);
+    nb.start[y] = st;
+    nb.count[y] = __ldcg(&na.count[x]);
+    nb.flags[y] = __ldcg(&na.flags[x]);
+    nb.level[y] = static_cast<std::uint8_t>(l);
+    nb.split[y] = __ldcg(&na.split[x]);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      nb.lo[static_cast<std::uint64_t>(y) * D + j] = __ldcg(&na.lo[static_cast<std::uint64_t>(x) * D + j]);
+      nb.hi[static_cast<std::uint64_t>(y) * D + j] = __ldcg(&na.hi[static_cast<std::uint64_t>(x) * D + j]);
+    }
+  }
+  // scatter the subtrees' nodes: one warp per subtree, level by level
+  for (std::uint32_t r = gwarp; r < R; r += nwarps) {
+    const std::uint32_t g = __ldcg(&a.small_list[r]);
+    const std::uint32_t rs = __ldcg(&na.start[g]);
+    const int L = __ldcg(&na.level[g]);
+    const int nlev = static_cast<int>(__ldcg(&a.sub_nlev[r]));
+    const std::uint32_t k = root_rank(rs);
+    std::uint32_t src = __ldcg(&a.sub_base[r]);
+    for (int lam = 1; lam < nlev; ++lam) {
+      const int l = L + lam;
+      const std::uint32_t cnt = __ldcg(&a.sub_cnt[static_cast<std::uint64_t>(r) * kSubLevels + lam]);
+      const std::uint32_t row = (l - Lmin - 1) * R;
+      std::uint32_t y0 = __ldcg(&a.new_off[l]) + __ldcg(&a.V[row + k]) - __ldcg(&a.V[row]);
+      if (l < HA) y0 += lower_bound_u32(na.start, __ldcg(&a.lvl_off[l]), __ldcg(&a.lvl_off[l + 1]), rs) - __ldcg(&a.lvl_off[l]);
+      for (std::uint32_t j = lane; j < cnt; j += 32) {
+        const std::uint32_t xs = src + j, y = y0 + j;
+        GK_ASSERT(y < 2 * n - 1 && xs < 2 * n);
+        nb.start[y] = __ldcg(&a.s_start[xs]);
+        nb.count[y] = __ldcg(&a.s_count[xs]);
+        nb.flags[y] = __ldcg(&a.s_flags[xs]);
+        nb.level[y] = static_cast<std::uint8_t>(l);
+        nb.split[y] = __ldcg(&a.s_split[xs]);
+#pragma unroll
+        for (int jj = 0; jj < D; ++jj) {
+          nb.lo[static_cast<std::uint64_t>(y) * D + jj] = __ldcg(&a.s_lo[static_cast<std::uint64_t>(xs) * D + jj]);
+          nb.hi[static_cast<std::uint64_t>(y) * D + jj] = __ldcg(&a.s_hi[static_cast<std::uint64_t>(xs) * D + jj]);
+        }
+      }
+      src += cnt;
+    }
+  }
+  sync_all(grid);
+  // parent / first child (or, for a leaf, the insertion point among the next level) by start
+  const std::uint32_t Nall = __ldcg(&a.new_off[H]);
+  for (std::uint32_t x = gtid; x < Nall; x += gthreads) {
+    const int l = __ldcg(&nb.level[x]);
+    const std::uint32_t st = __ldcg(&nb.start[x]);
+    GK_ASSERT(l < H && st < n);
+    const std::uint32_t o1 = __ldcg(&a.new_off[l + 1]), o2 = __ldcg(&a.new_off[l + 2 <= H ? l + 2 : H]);
+    nb.cbase[x] = (l + 1 < H) ? lower_bound_u32(nb.start, o1, o2, st) : o1;
+    if (l == 0) {
+      nb.parent[x] = 0xffffffffu;
+    } else {
+      const std::uint32_t p0 = __ldcg(&a.new_off[l - 1]);
+      nb.parent[x] = lower_bound_u32(nb.start, p0, __ldcg(&a.new_off[l]), st + 1) - 1;  // last start <= st
+    }
+  }
+  sync_all(grid);
+  veb_phase(grid, a, nb, a.new_off, H);
 }
 
 __global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::uint32_t* irank_by_slot) {
@@ -1077,8 +1649,9 @@ int capacity_d() {
   static int maxb[kMaxDevices] = {};  // per D and device
   const int dev = current_device();
   if (!maxb[dev])
-    maxb[dev] = std::min(coresident_blocks(reinterpret_cast<const void*>(k_build<D, 0>)),
-                         coresident_blocks(reinterpret_cast<const void*>(k_build<D, 1>)));
+    maxb[dev] = std::min(std::min(coresident_blocks(reinterpret_cast<const void*>(k_build<D, 0>)),
+                                  coresident_blocks(reinterpret_cast<const void*>(k_build<D, 1>))),
+                         coresident_blocks(reinterpret_cast<const void*>(k_merge<D>)));
   return maxb[dev];
 }
 
@@ -1098,6 +1671,14 @@ std::size_t scratch_bytes(std::uint64_t n, std::uint64_t cap_chunks, int G) {
          kSelCap * 256 * 4 + (2 * G + 2) * 4 + 4 * (cap + 1) + 40 * 256;
 }
 
+// the bottom phase's arrays (small roots, subtree node records, merge scratch, merged level arrays)
+template <int D>
+std::size_t bottom_bytes(std::uint64_t n, int leaf) {
+  const std::uint64_t cap = 2 * n - 1, rmax = n / (leaf + 1) + 1;
+  return rmax * 4 * 4 + rmax * kSubLevels * 4 + 2 * n * (4 + 4 + 4 + 1 + 8 + 16 * D) + 2 * (n + 1) * 4 +
+         (rmax * kVLevels + 1) * 4 + (kMaxLevels + 2) * 4 + cap * (4 + 4 + 1 + 1 + 8 + 16 * D) + 16 * 256;
+}
+
 // upper bound of the device memory one build allocates: its scratch (at the smallest chunk size) plus
 // the tree it leaves behind (coordinates, ids, canonical + traversal nodes, topology, ranks)
 template <int D>
@@ -1105,7 +1686,8 @@ std::size_t build_bytes_d(std::uint64_t n) {
   if (n == 0) return 0;
   const std::uint64_t cap = 2 * n - 1;
   const std::size_t tree = n * (8 * D + 4) + cap * (sizeof(gk_canon_node) + 12 + 4) + (cap / 2 + 1) * sizeof(TNode<D>);
-  return scratch_bytes<D>(n, n / 32 + std::min<std::uint64_t>(cap, n) + 2, capacity_d<D>()) + tree + 8 * 4096;
+  return scratch_bytes<D>(n, n / 32 + std::min<std::uint64_t>(cap, n) + 2, capacity_d<D>()) + bottom_bytes<D>(n, 4) +
+         tree + 8 * 4096;
 }
 
 template <int D>
@@ -1143,7 +1725,13 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   a.src = src;
   a.src_stride = src_stride;
   a.src_ids = src_ids;
-  const std::size_t need = scratch_bytes<D>(n, cap_chunks, G);
+  // bottom phase: both heuristics, leaves of >= 4 points (the per-level node arrays of a subtree are
+  // sized for internal nodes of >= 5 points); GK_NO_SMALL=1 turns it off (A/B experiments)
+  static const bool no_small = std::getenv("GK_NO_SMALL") != nullptr;
+  static const std::uint64_t small_max_n = std::getenv("GK_SMALL_MAX_N") ? std::strtoull(std::getenv("GK_SMALL_MAX_N"), nullptr, 10)
+                                                                         : kSmallMaxN;
+  const bool bottom = !no_small && leaf >= 4 && leaf < small_cap<D>() && n <= small_max_n;
+  const std::size_t need = scratch_bytes<D>(n, cap_chunks, G) + (bottom ? bottom_bytes<D>(n, leaf) : 0);
   char* base = sc.reserve(need, st);
   std::size_t used = 0;
   auto take = [&](std::size_t bytes) -> char* {
@@ -1186,11 +1774,63 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   a.hist = reinterpret_cast<std::uint32_t*>(take(kSelCap * 256 * 4));
   a.bsum = reinterpret_cast<std::uint32_t*>(take((2 * G + 2) * 4));
   a.int_by_slot = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
+  a.Tsmall = bottom ? static_cast<std::uint32_t>(small_cap<D>()) : 0u;
+  if (bottom) {
+    const std::uint64_t rmax = n / (leaf + 1) + 1;
+    a.rmax = static_cast<std::uint32_t>(rmax);
+    a.small_list = reinterpret_cast<std::uint32_t*>(take(rmax * 4));
+    a.sub_base = reinterpret_cast<std::uint32_t*>(take(rmax * 4));
+    a.sub_nlev = reinterpret_cast<std::uint32_t*>(take(rmax * 4));
+    a.order = reinterpret_cast<std::uint32_t*>(take(rmax * 4));
+    a.sub_cnt = reinterpret_cast<std::uint32_t*>(take(rmax * kSubLevels * 4));
+    a.s_start = reinterpret_cast<std::uint32_t*>(take(2 * n * 4));
+    a.s_count = reinterpret_cast<std::uint32_t*>(take(2 * n * 4));
+    a.s_child = reinterpret_cast<std::uint32_t*>(take(2 * n * 4));
+    a.s_flags = reinterpret_cast<std::uint8_t*>(take(2 * n));
+    a.s_split = reinterpret_cast<double*>(take(2 * n * 8));
+    a.s_lo = reinterpret_cast<double*>(take(2 * n * D * 8));
+    a.s_hi = reinterpret_cast<double*>(take(2 * n * D * 8));
+    a.marks = reinterpret_cast<std::uint32_t*>(take((n + 1) * 4));
+    a.mscan = reinterpret_cast<std::uint32_t*>(take((n + 1) * 4));
+    a.vcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(rmax * kVLevels, 0xfffffff0ULL));
+    a.V = reinterpret_cast<std::uint32_t*>(take((static_cast<std::uint64_t>(a.vcap) + 1) * 4));
+    a.new_off = reinterpret_cast<std::uint32_t*>(take((kMaxLevels + 2) * 4));
+    NodeArrays& nb = a.na2;
+    nb.start = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+    nb.count = reinterpret_cast<std::uint32_t*>(take(cap * 4));
+    nb.flags = reinterpret_cast<std::uint8_t*>(take(cap));
+    nb.level = reinterpret_cast<std::uint8_t*>(take(cap));
+    nb.split = reinterpret_cast<double*>(take(cap * 8));
+    nb.lo = reinterpret_cast<double*>(take(cap * D * 8));
+    nb.hi = reinterpret_cast<double*>(take(cap * D * 8));
+    nb.parent = na.parent;  // recomputed by k_merge; the level loop's values are dead by then
+    nb.cbase = na.cbase;
+    nb.pos = na.pos;
+    nb.nleft = na.nleft;
+    nb.thr_id = na.thr_id;
+  }
   if (used > need) throw Error(GK_ERR_LOGIC, "BuildvEB_S scratch accounting");
 
   void* args[] = {&a};
   GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D, 0>), dim3(G), dim3(kThreads), args, 0, st));
   GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_build<D, 1>), dim3(G), dim3(kThreads), args, 0, st));
+  if (bottom) {  // the subtrees of the small nodes (one block each), then the merge + vEB phase
+    static std::once_flag once[kMaxDevices];
+    static int sub_resident[kMaxDevices] = {};
+    const int dev = current_device();
+    std::call_once(once[dev], [&] {
+      GK_CUDA(cudaFuncSetAttribute(k_subtree<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(small_smem<D>())));
+      int sms = 0, per = 0;
+      GK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_subtree<D>, kSubThreads, small_smem<D>()));
+      sub_resident[dev] = std::max(1, per) * sms;
+    });
+    const unsigned sg = static_cast<unsigned>(std::min<std::uint64_t>(sub_resident[dev], n / (leaf + 1) + 1));
+    k_subtree<D><<<sg, kSubThreads, small_smem<D>(), st>>>(a);
+    GK_CHECK_LAUNCH();
+    GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_merge<D>), dim3(G), dim3(kThreads), args, 0, st));
+  }
   GK_CUDA(cudaMemcpyAsync(sc.host_ctrl, a.ctrl, C_COUNT * 4, cudaMemcpyDeviceToHost, st));
   sc.d = D;
   sc.grid = G;
@@ -1224,7 +1864,9 @@ void build_finish_d(BuildScratch& sc) {
   void* args2[] = {&a, &irank_ptr};
   const int G2 = static_cast<int>(std::min<std::uint64_t>(G, std::max<std::uint64_t>(1, N / 4096)));
   GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_slot_rank), dim3(G2), dim3(kThreads), args2, 0, st));
-  k_emit<D><<<blocks_for(N), 256, 0, st>>>(a, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
+  BuildArgs ea = a;  // after the bottom phase the merged level arrays are a.na2
+  if (sc.host_ctrl[C_NSMALL] > 0) ea.na = a.na2;
+  k_emit<D><<<blocks_for(N), 256, 0, st>>>(ea, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
   GK_CHECK_LAUNCH();
   T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
   T.root_slot = 0;

@@ -155,7 +155,7 @@ struct BuildScratch {
   void* base = nullptr;
   std::size_t size = 0;
   std::uint32_t* host_ctrl = nullptr;
-  alignas(16) unsigned char args[640];  // the in-flight build's kernel arguments
+  alignas(16) unsigned char args[1024];  // the in-flight build's kernel arguments
   int d = 0, grid = 0;
   std::uint64_t n = 0;
   DevTree* out = nullptr;
