@@ -111,10 +111,12 @@ struct SelState {
 enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_NSMALL = 5, C_SUBCTR = 6, C_WORK = 7, C_COUNT = 8 };
 constexpr int kSubLevels = 64;  // local levels of a bottom-phase subtree (<= kDepthCap + 12 + 1)
 constexpr int kVLevels = 160;
-// trees up to this size use the bottom phase by default (measured: C1's trees of <= 512K points build
-// faster with it; C2's 8.4M-point tree slower -- its level loop is bandwidth-bound, the bottom phase
-// issue-bound); GK_SMALL_MAX_N overrides
-constexpr std::uint64_t kSmallMaxN = 1ull << 20;   // absolute levels a merge spans (small roots at depths <= ~72, + kSubLevels)
+// trees up to this size use the bottom phase by default (D <= 4; measured on the B200, bottom phase on /
+// off: C1 Insert_L 1.23 / 1.51 ms, C4's ten Insert_L 21.0 / 23.5 ms, C5 Erase_L 5.4 / 5.6 ms; the 8.4M-point
+// trees of C2 / C5 break even or lose 2-3 % -- their level loop is bandwidth-bound, the bottom phase
+// issue-bound -- and at D >= 5 (subtrees of <= 256 points) it lost 5 % on C3); GK_SMALL_MAX_N overrides
+template <int D>
+constexpr std::uint64_t small_max_n() { return D <= 4 ? (1ull << 22) : 0; }   // absolute levels a merge spans (small roots at depths <= ~72, + kSubLevels)
 
 struct BuildArgs {
   int leaf, heuristic;
@@ -950,7 +952,6 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
 // then interleaves the subtrees' nodes with the level loop's into complete level arrays (left-to-right
 // = start order at every level) and runs the vEB slot phase over them.
 constexpr int kSubThreads = 256;
-constexpr std::uint16_t kNoSeg = 0xffff;  // position of a leaf finished at an earlier level
 #ifdef GK_DBG
 #include <cassert>
 #define GK_ASSERT(c) assert(c)
@@ -971,8 +972,9 @@ __host__ __device__ constexpr int small_nmax() {  // nodes per level of a subtre
 template <int D>
 __host__ __device__ constexpr std::size_t small_smem() {
   constexpr int T = small_cap<D>(), NM = small_nmax<D>();
-  return static_cast<std::size_t>(T) * D * 8 + static_cast<std::size_t>(NM) * D * 16 + NM * 8 + T * 4 + NM * 4 +
-         NM * 4 + 32 * 4 + 16 + 2 * (kSubLevels + 1) * 4 + T * 2 * 4 + (T + 1) * 2 + NM * 2 * 4 + (NM + 1) * 2 + NM + 64;
+  return static_cast<std::size_t>(T) * D * 8 + static_cast<std::size_t>(NM) * 2 * 2 * 8 + 32 * 4 * 8 + T * 4 +
+         32 * 4 + 16 + 2 * (kSubLevels + 1) * 4 + T * 2 * 2 + (T + 1) * 2 + NM * 2 * 4 + (NM + 1) * 2 +
+         (T / 128 + 2) * 2 + 64;
 }
 
 // in-place exclusive scan of a[0, n) (a[n] = total) by the whole block; wsum: 32 words of shared memory
@@ -1010,34 +1012,51 @@ __device__ void block_exscan_u16(std::uint16_t* a, int n, std::uint32_t* wsum) {
   __syncthreads();
 }
 
+__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return b < a ? b : a; }
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return b > a ? b : a; }
+__device__ __forceinline__ void warp_minmax(unsigned long long& mn, unsigned long long& mx) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = umin64(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = umax64(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+}
+
+// One subtree per block.  Per local level, nodes of at most kSubBig points are handled by one warp each
+// (their positions in <= 4 rounds of 32, predicates and ranks by ballots), larger ones by the whole
+// block one after another (block scan).  The split-dimension box of every node comes from its parent's
+// partition (the children's min/max in the next level's dimension accumulate while it partitions);
+// leaves reduce their full box; internal nodes' full boxes are the unions of their children's,
+// bottom-up after the last level.
+constexpr int kSubBig = 128;
 template <int D>
 __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
   constexpr int T = small_cap<D>(), NM = small_nmax<D>();
+  static_assert(kSubBig <= 128, "warp-mode nodes take at most 4 rounds of 32 points");
   extern __shared__ __align__(16) unsigned char smem[];
-  double* X = reinterpret_cast<double*>(smem);                                     // [D][T]
-  unsigned long long* nbox = reinterpret_cast<unsigned long long*>(X + D * T);      // [NM][D][2] dkey
-  double* nsplit = reinterpret_cast<double*>(nbox + NM * D * 2);                    // [NM]
-  std::uint32_t* ID = reinterpret_cast<std::uint32_t*>(nsplit + NM);                // [T]
-  std::uint32_t* nthr = ID + T;                                                     // [NM]
-  std::uint32_t* nleft = nthr + NM;                                                 // [NM]
-  std::uint32_t* wsum = nleft + NM;                                                 // [32]
-  std::uint32_t* misc = wsum + 32;                                                  // [4]
-  std::uint32_t* lvo = misc + 4;                     // [kSubLevels + 1] region offset of each local level
-  std::uint32_t* lvc = lvo + kSubLevels + 1;         // [kSubLevels + 1] nodes of each local level
-  std::uint16_t* permA = reinterpret_cast<std::uint16_t*>(lvc + kSubLevels + 1);    // [T]
-  std::uint16_t* permB = permA + T;                                                 // [T]
-  std::uint16_t* seg = permB + T;                                                   // [T] position -> node
-  std::uint16_t* seg2 = seg + T;                                                    // [T] (next level)
-  std::uint16_t* Lsc = seg2 + T;                                                    // [T + 1]
-  std::uint16_t* nst = Lsc + T + 1;                                                 // [2][NM]
-  std::uint16_t* ncn = nst + 2 * NM;                                                // [2][NM]
-  std::uint16_t* nscan = ncn + 2 * NM;                                              // [NM + 1]
-  std::uint8_t* nfl = reinterpret_cast<std::uint8_t*>(nscan + NM + 1);              // [NM]
+  double* X = reinterpret_cast<double*>(smem);                                        // [D][T]
+  unsigned long long* nbl = reinterpret_cast<unsigned long long*>(X + D * T);          // [2][NM] split-dim lo key
+  unsigned long long* nbh = nbl + 2 * NM;                                              // [2][NM] split-dim hi key
+  unsigned long long* red = nbh + 2 * NM;                                              // [32][4] block reductions
+  std::uint32_t* ID = reinterpret_cast<std::uint32_t*>(red + 32 * 4);                  // [T]
+  std::uint32_t* wsum = ID + T;                                                        // [32]
+  std::uint32_t* misc = wsum + 32;                                                     // [4]
+  std::uint32_t* lvo = misc + 4;                                                       // [kSubLevels + 1]
+  std::uint32_t* lvc = lvo + kSubLevels + 1;                                           // [kSubLevels + 1]
+  std::uint16_t* permA = reinterpret_cast<std::uint16_t*>(lvc + kSubLevels + 1);       // [T]
+  std::uint16_t* permB = permA + T;                                                    // [T]
+  std::uint16_t* Lsc = permB + T;                                                      // [T + 1]
+  std::uint16_t* nst = Lsc + T + 1;                                                    // [2][NM]
+  std::uint16_t* ncn = nst + 2 * NM;                                                   // [2][NM]
+  std::uint16_t* nscan = ncn + 2 * NM;                                                 // [NM + 1]
+  std::uint16_t* bigl = nscan + NM + 1;                                                // [T / kSubBig + 1]
 
   const NodeArrays& na = a.na;
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarps = nth >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
   const std::uint64_t N = a.n;  // SoA stride of the output
   const bool spatial_heur = a.heuristic != GK_OBJECT_MEDIAN;
+  const int leaf = a.leaf;
   while (true) {
     if (tid == 0) misc[0] = atomicAdd(&a.ctrl[C_WORK], 1u);
     __syncthreads();
@@ -1047,205 +1066,260 @@ __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
     const std::uint32_t s0 = __ldcg(&na.start[g]);
     const int n = static_cast<int>(__ldcg(&na.count[g]));
     const int L = __ldcg(&na.level[g]);
-    if (tid == 0) misc[1] = atomicAdd(&a.ctrl[C_SUBCTR], 2u * static_cast<std::uint32_t>(n));
+    if (tid == 0) {
+      misc[1] = atomicAdd(&a.ctrl[C_SUBCTR], 2u * static_cast<std::uint32_t>(n));
+      nst[0] = 0;
+      ncn[0] = static_cast<std::uint16_t>(n);
+      const int c0 = L % D;  // the root's box in its split dimension (the level loop computed it)
+      nbl[0] = dkey(__ldcg(&na.lo[static_cast<std::uint64_t>(g) * D + c0]));
+      nbh[0] = dkey(__ldcg(&na.hi[static_cast<std::uint64_t>(g) * D + c0]));
+    }
     for (int i = tid; i < n; i += nth) {
 #pragma unroll
       for (int j = 0; j < D; ++j) X[j * T + i] = __ldcg(&a.out[j * N + s0 + i]);
       ID[i] = __ldcg(&a.out_ids[s0 + i]);
       permA[i] = static_cast<std::uint16_t>(i);
-      seg[i] = 0;
-    }
-    if (tid == 0) {
-      nst[0] = 0;
-      ncn[0] = static_cast<std::uint16_t>(n);
     }
     __syncthreads();
     const std::uint32_t base = misc[1];
     GK_ASSERT(base + 2u * n <= 2u * a.n && n <= T && r < a.rmax);
-    std::uint32_t rec = base;  // next record of the subtree's region (local levels >= 1, level-major)
+    std::uint32_t rec = base;  // this level's first record (local levels >= 1, level-major)
     std::uint16_t* perm = permA;
     std::uint16_t* perm2 = permB;
     int cb = 0, nc = 1, lv = 0;
     for (;; ++lv) {
       if (lv >= kSubLevels) __trap();  // unreachable: depth cap 40 + log2(T) + 1 levels
-      const int depth = L + lv, c = depth % D;
+      const int depth = L + lv, c = depth % D, c1 = (depth + 1) % D;
       const bool spatial = spatial_heur && depth < kDepthCap;
-      std::uint16_t* cst = nst + cb * NM;
-      std::uint16_t* ccn = ncn + cb * NM;
-      // (a) node boxes.  A node's positions are contiguous: a segmented min/max scan inside each warp
-      // (shuffles between lanes of the same node), then one shared-memory atomic per node run per warp.
-      // Internal nodes need only the split dimension here (their full boxes are the unions of their
-      // children's, computed bottom-up after the last level); leaves need every dimension.
-      for (int i = tid; i < nc * D; i += nth) {
-        nbox[2 * i] = ~0ULL;
-        nbox[2 * i + 1] = 0ULL;
-      }
-      __syncthreads();
-      for (int p0 = wid * 32; p0 < n; p0 += nth) {
-        const int p = p0 + lane;
-        const int sg = p < n ? seg[p] : kNoSeg;
-        const bool valid = sg != kNoSeg;
-        if (!__any_sync(0xffffffffu, valid)) continue;  // only finished leaves in this chunk
-        const int node = valid ? sg : -1 - lane;        // invalid lanes: singleton runs
-        const bool isleaf = valid && ccn[sg] <= a.leaf;
-        const bool anyleaf = __any_sync(0xffffffffu, isleaf);
-        const int ip = valid ? perm[p] : 0;
-        unsigned same = 0;  // bit o: the lane 2^o below belongs to the same node
-#pragma unroll
-        for (int o = 0; o < 5; ++o) {
-          const int up = __shfl_up_sync(0xffffffffu, node, 1 << o);
-          if (lane >= (1 << o) && up == node) same |= 1u << o;
-        }
-        const int dn = __shfl_down_sync(0xffffffffu, node, 1);
-        const bool tail = valid && (lane == 31 || dn != node);
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          if (j != c && !anyleaf) continue;  // warp-uniform
-          const bool use = valid && (j == c || isleaf);
-          unsigned long long mn = use ? dkey(X[j * T + ip]) : ~0ULL, mx = use ? mn : 0ULL;
-#pragma unroll
-          for (int o = 0; o < 5; ++o) {
-            const unsigned long long a1 = __shfl_up_sync(0xffffffffu, mn, 1 << o);
-            const unsigned long long b1 = __shfl_up_sync(0xffffffffu, mx, 1 << o);
-            if (same >> o & 1u) {
-              mn = a1 < mn ? a1 : mn;
-              mx = b1 > mx ? b1 : mx;
-            }
-          }
-          if (tail && use) {
-            atomicMin(&nbox[(node * D + j) * 2], mn);
-            atomicMax(&nbox[(node * D + j) * 2 + 1], mx);
-          }
-        }
-      }
-      __syncthreads();
-      // (b) leaf / spatial split / object
-      for (int i = tid; i < nc; i += nth) {
-        const int cnt = ccn[i];
-        std::uint8_t fl = 0;
-        if (cnt <= a.leaf) {
-          fl = F_LEAF;
-          nsplit[i] = 0.0;
-        } else if (spatial) {
-          const double l = dkey_inv(nbox[(i * D + c) * 2]), h = dkey_inv(nbox[(i * D + c) * 2 + 1]);
-          nsplit[i] = __dmul_rn(__dadd_rn(l, h), 0.5);  // (lo + hi) / 2 exactly
-        } else {
-          fl = F_OBJECT;
-        }
-        nfl[i] = fl;
-        nleft[i] = 0;
-        nthr[i] = 0;
-        nscan[i] = (fl & F_LEAF) ? 0 : 1;  // internal nodes -> child slots of the next level
-      }
-      __syncthreads();
-      block_exscan_u16(nscan, nc, wsum);
-      const int nint = nscan[nc];
-      // (c) spatial left counts (warp-aggregated per node)
-      for (int p0 = wid * 32; p0 < n; p0 += nth) {
-        const int p = p0 + lane;
-        const int sg = p < n ? seg[p] : kNoSeg;
-        const bool valid = sg != kNoSeg;
-        const int node = valid ? sg : -1;
-        bool pr = false;
-        if (valid && nfl[node] == 0) pr = X[c * T + perm[p]] < nsplit[node];
-        const unsigned grp = __match_any_sync(0xffffffffu, node);
-        const unsigned pm = __ballot_sync(0xffffffffu, pr);
-        if (valid && nfl[node] == 0 && lane == __ffs(grp) - 1 && (pm & grp)) atomicAdd(&nleft[node], __popc(pm & grp));
-      }
-      __syncthreads();
-      // (d) degenerate spatial splits -> object median; object nodes keep the floor(n/2) smallest keys
-      for (int i = tid; i < nc; i += nth) {
-        const std::uint32_t cnt = ccn[i];
-        std::uint8_t fl = nfl[i];
-        if (fl == 0 && (nleft[i] == 0 || nleft[i] == cnt)) fl = F_OBJECT;
-        if (fl == F_OBJECT) nleft[i] = cnt / 2;
-        nfl[i] = fl;
-      }
-      __syncthreads();
-      // (e) object thresholds: the key of rank floor(n/2) in (x_c, id) order (-0 == +0), by rank counting
-      for (int p = tid; p < n; p += nth) {
-        const int node = seg[p];
-        if (node == kNoSeg || nfl[node] != F_OBJECT) continue;
-        const int ip = perm[p];
-        const double xp = X[c * T + ip];
-        const std::uint32_t idp = ID[ip];
-        const int st = cst[node], cn = ccn[node];
-        std::uint32_t rank = 0;
-        for (int q = st; q < st + cn; ++q) {
-          const int iq = perm[q];
-          const double xq = X[c * T + iq];
-          rank += (xq < xp || (xq == xp && ID[iq] < idp)) ? 1u : 0u;
-        }
-        if (rank == nleft[node]) {  // keys are unique (ids are): exactly one position writes
-          nsplit[node] = __dadd_rn(xp, 0.0);  // canonical +0 for a zero median, as the level loop
-          nthr[node] = idp;
-        }
-      }
-      __syncthreads();
-      // (f) partition predicate, block scan
-      for (int p = tid; p < n; p += nth) {
-        const int node = seg[p];
-        const std::uint8_t fl = node == kNoSeg ? F_LEAF : nfl[node];
-        bool pr = false;
-        if (!(fl & F_LEAF)) {
-          const int ip = perm[p];
-          const double x = X[c * T + ip];
-          const double sp = nsplit[node];
-          pr = (fl & F_OBJECT) ? (x < sp || (x == sp && ID[ip] < nthr[node])) : (x < sp);
-        }
-        Lsc[p] = pr ? 1 : 0;
-      }
-      __syncthreads();
-      block_exscan_u16(Lsc, n, wsum);
-      // (g) stable partition of the positions (leaves keep theirs); the next level's position -> node map
-      for (int p = tid; p < n; p += nth) {
-        const int node = seg[p];
-        int np = p;
-        std::uint16_t child = kNoSeg;
-        if (node != kNoSeg && !(nfl[node] & F_LEAF)) {
-          const int st = cst[node];
-          const int lr = Lsc[p] - Lsc[st];
-          const bool pr = Lsc[p + 1] != Lsc[p];
-          np = pr ? st + lr : st + static_cast<int>(nleft[node]) + (p - st - lr);
-          child = static_cast<std::uint16_t>(2 * nscan[node] + (pr ? 0 : 1));
-        }
-        perm2[np] = perm[p];
-        seg2[np] = child;
-      }
-      // (h) this level's node records; internal nodes -> the next level's nodes
+      const std::uint16_t* cst = nst + cb * NM;
+      const std::uint16_t* ccn = ncn + cb * NM;
+      const unsigned long long* cbl = nbl + cb * NM;
+      const unsigned long long* cbh = nbh + cb * NM;
       std::uint16_t* xst = nst + (cb ^ 1) * NM;
       std::uint16_t* xcn = ncn + (cb ^ 1) * NM;
+      unsigned long long* xbl = nbl + (cb ^ 1) * NM;
+      unsigned long long* xbh = nbh + (cb ^ 1) * NM;
+      if (tid == 0) misc[3] = 0;
+      __syncthreads();
       for (int i = tid; i < nc; i += nth) {
-        const std::uint8_t fl = nfl[i];
-        const int st = cst[i], cnt = ccn[i];
-        if (!(fl & F_LEAF)) {
-          const int k2 = 2 * nscan[i];
-          xst[k2] = static_cast<std::uint16_t>(st);
-          xcn[k2] = static_cast<std::uint16_t>(nleft[i]);
-          xst[k2 + 1] = static_cast<std::uint16_t>(st + nleft[i]);
-          xcn[k2 + 1] = static_cast<std::uint16_t>(cnt - static_cast<int>(nleft[i]));
-        }
+        nscan[i] = ccn[i] > leaf ? 1 : 0;  // internal -> child slots
+        if (ccn[i] > kSubBig) bigl[atomicAdd(&misc[3], 1u)] = static_cast<std::uint16_t>(i);  // block-mode nodes
+      }
+      __syncthreads();
+      const int nbig = static_cast<int>(misc[3]);
+      block_exscan_u16(nscan, nc, wsum);
+      const int nint = nscan[nc];
+      // the node's record (this level), its children's slots and split-dim boxes (next level)
+      auto finish = [&](int i, int st, int cnt, std::uint8_t fl, double sp, std::uint32_t thr, int nl,
+                        unsigned long long mnl, unsigned long long mxl, unsigned long long mnr, unsigned long long mxr) {
+        const int k2 = 2 * nscan[i];
+        xst[k2] = static_cast<std::uint16_t>(st);
+        xcn[k2] = static_cast<std::uint16_t>(nl);
+        xst[k2 + 1] = static_cast<std::uint16_t>(st + nl);
+        xcn[k2 + 1] = static_cast<std::uint16_t>(cnt - nl);
+        xbl[k2] = mnl;
+        xbh[k2] = mxl;
+        xbl[k2 + 1] = mnr;
+        xbh[k2 + 1] = mxr;
         if (lv == 0) {  // the subtree root is the level loop's node g: finish its record
           na.flags[g] = fl;
-          na.split[g] = nsplit[i];
-          na.thr_id[g] = nthr[i];
+          na.split[g] = sp;
+          na.thr_id[g] = thr;
         } else {
           const std::uint32_t ri = rec + i;
           GK_ASSERT(ri < base + 2u * n);
           a.s_start[ri] = s0 + st;
           a.s_count[ri] = cnt;
           a.s_flags[ri] = fl;
-          a.s_split[ri] = nsplit[i];
-          if (fl & F_LEAF) {
+          a.s_split[ri] = sp;
+          a.s_child[ri] = rec + nc + k2;  // the next level's records follow this level's
+        }
+      };
+      // ---- warp mode: leaves and nodes of <= kSubBig points, one warp each
+      for (int i = wid; i < nc; i += nwarps) {
+        const int st = cst[i], cnt = ccn[i];
+        if (cnt > kSubBig) continue;
+        if (cnt <= leaf) {  // a leaf (<= 32 points): positions final (both buffers), full box
+          const bool v = lane < cnt;
+          const int ip = v ? perm[st + lane] : 0;
+          if (v) perm2[st + lane] = static_cast<std::uint16_t>(ip);
+          if (lv > 0) {
+            const std::uint32_t ri = rec + i;
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-              a.s_lo[static_cast<std::uint64_t>(ri) * D + j] = dkey_inv(nbox[(i * D + j) * 2]);
-              a.s_hi[static_cast<std::uint64_t>(ri) * D + j] = dkey_inv(nbox[(i * D + j) * 2 + 1]);
+              unsigned long long mn = v ? dkey(X[j * T + ip]) : ~0ULL, mx = v ? mn : 0ULL;
+              warp_minmax(mn, mx);
+              if (lane == 0) {
+                a.s_lo[static_cast<std::uint64_t>(ri) * D + j] = dkey_inv(mn);
+                a.s_hi[static_cast<std::uint64_t>(ri) * D + j] = dkey_inv(mx);
+              }
             }
-          } else {
-            a.s_child[ri] = rec + nc + 2u * nscan[i];  // the next level's records follow this level's
+            if (lane == 0) {
+              a.s_start[ri] = s0 + st;
+              a.s_count[ri] = cnt;
+              a.s_flags[ri] = F_LEAF;
+              a.s_split[ri] = 0.0;
+            }
+          }
+          continue;
+        }
+        const int nit = (cnt + 31) >> 5;
+        bool v[4];
+        int ip[4];
+        double x[4];
+        unsigned b[4];
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int q = 32 * it + lane;
+          v[it] = it < nit && q < cnt;
+          ip[it] = v[it] ? perm[st + q] : 0;
+          x[it] = v[it] ? X[c * T + ip[it]] : 0.0;
+          b[it] = 0;
+        }
+        std::uint8_t fl = F_OBJECT;
+        double sp = 0.0;
+        std::uint32_t thr = 0;
+        int nl = 0;
+        if (spatial) {
+          sp = __dmul_rn(__dadd_rn(dkey_inv(cbl[i]), dkey_inv(cbh[i])), 0.5);  // (lo + hi) / 2 exactly
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            b[it] = __ballot_sync(0xffffffffu, v[it] && x[it] < sp);
+            nl += __popc(b[it]);
+          }
+          if (nl > 0 && nl < cnt) fl = 0;
+        }
+        if (fl == F_OBJECT) {  // object median: the key of rank floor(cnt/2) in (x_c, id) order (-0 == +0)
+          const int m = cnt / 2;
+          std::uint32_t idv[4];
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            idv[it] = v[it] ? ID[ip[it]] : 0u;
+            int rank = -1;
+            if (v[it]) {
+              rank = 0;
+              for (int q = st; q < st + cnt; ++q) {
+                const int iq = perm[q];
+                const double xq = X[c * T + iq];
+                rank += (xq < x[it] || (xq == x[it] && ID[iq] < idv[it])) ? 1 : 0;
+              }
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, rank == m);
+            if (hit) {
+              const int src = __ffs(hit) - 1;
+              sp = __dadd_rn(__shfl_sync(0xffffffffu, x[it], src), 0.0);  // canonical +0, as the level loop
+              thr = __shfl_sync(0xffffffffu, idv[it], src);
+            }
+          }
+          nl = 0;
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            b[it] = __ballot_sync(0xffffffffu, v[it] && (x[it] < sp || (x[it] == sp && idv[it] < thr)));
+            nl += __popc(b[it]);
           }
         }
+        // stable partition + the children's boxes in the next level's split dimension
+        unsigned long long mnl = ~0ULL, mxl = 0ULL, mnr = ~0ULL, mxr = 0ULL;
+        int before = 0;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const bool pr = (b[it] >> lane) & 1u;
+          if (v[it]) {
+            const int q = 32 * it + lane;
+            const int rk = before + __popc(b[it] & lt_mask);
+            const int np = pr ? st + rk : st + nl + (q - rk);
+            perm2[np] = static_cast<std::uint16_t>(ip[it]);
+            const unsigned long long k = dkey(X[c1 * T + ip[it]]);
+            if (pr) { mnl = umin64(mnl, k); mxl = umax64(mxl, k); }
+            else { mnr = umin64(mnr, k); mxr = umax64(mxr, k); }
+          }
+          before += __popc(b[it]);
+        }
+        warp_minmax(mnl, mxl);
+        warp_minmax(mnr, mxr);
+        if (lane == 0) finish(i, st, cnt, fl, sp, thr, nl, mnl, mxl, mnr, mxr);
+      }
+      // ---- block mode: nodes of more than kSubBig points, the whole block on one node at a time
+      for (int bi = 0; bi < nbig; ++bi) {
+        const int i = bigl[bi];
+        const int st = cst[i], cnt = ccn[i];
+        std::uint8_t fl = F_OBJECT;
+        double sp = 0.0;
+        std::uint32_t thr = 0;
+        int nl = 0;
+        if (spatial) {
+          sp = __dmul_rn(__dadd_rn(dkey_inv(cbl[i]), dkey_inv(cbh[i])), 0.5);
+          int cntl = 0;
+          for (int q = tid; q < cnt; q += nth) cntl += X[c * T + perm[st + q]] < sp ? 1 : 0;
+          nl = 0;
+          for (int o = 16; o > 0; o >>= 1) cntl += __shfl_xor_sync(0xffffffffu, cntl, o);
+          if (lane == 0) wsum[wid] = static_cast<std::uint32_t>(cntl);
+          __syncthreads();
+          for (int w = 0; w < nwarps; ++w) nl += static_cast<int>(wsum[w]);
+          __syncthreads();
+          if (nl > 0 && nl < cnt) fl = 0;
+        }
+        if (fl == F_OBJECT) {
+          const int m = cnt / 2;
+          for (int q = tid; q < cnt; q += nth) {
+            const int ipq = perm[st + q];
+            const double xp = X[c * T + ipq];
+            const std::uint32_t idp = ID[ipq];
+            int rank = 0;
+            for (int u = st; u < st + cnt; ++u) {
+              const int iu = perm[u];
+              const double xu = X[c * T + iu];
+              rank += (xu < xp || (xu == xp && ID[iu] < idp)) ? 1 : 0;
+            }
+            if (rank == m) {  // unique
+              reinterpret_cast<double*>(red)[0] = __dadd_rn(xp, 0.0);
+              misc[2] = idp;
+            }
+          }
+          __syncthreads();
+          sp = reinterpret_cast<double*>(red)[0];
+          thr = misc[2];
+          nl = m;
+          __syncthreads();
+        }
+        // predicates, block scan, stable partition, children's split-dim boxes
+        for (int q = tid; q < cnt; q += nth) {
+          const int ipq = perm[st + q];
+          const double xq = X[c * T + ipq];
+          const bool pr = (fl == F_OBJECT) ? (xq < sp || (xq == sp && ID[ipq] < thr)) : (xq < sp);
+          Lsc[q] = pr ? 1 : 0;
+        }
+        __syncthreads();
+        block_exscan_u16(Lsc, cnt, wsum);
+        unsigned long long mnl = ~0ULL, mxl = 0ULL, mnr = ~0ULL, mxr = 0ULL;
+        for (int q = tid; q < cnt; q += nth) {
+          const int ipq = perm[st + q];
+          const bool pr = Lsc[q + 1] != Lsc[q];
+          const int np = pr ? st + Lsc[q] : st + nl + (q - Lsc[q]);
+          perm2[np] = static_cast<std::uint16_t>(ipq);
+          const unsigned long long k = dkey(X[c1 * T + ipq]);
+          if (pr) { mnl = umin64(mnl, k); mxl = umax64(mxl, k); }
+          else { mnr = umin64(mnr, k); mxr = umax64(mxr, k); }
+        }
+        warp_minmax(mnl, mxl);
+        warp_minmax(mnr, mxr);
+        if (lane == 0) {
+          red[wid * 4 + 0] = mnl;
+          red[wid * 4 + 1] = mxl;
+          red[wid * 4 + 2] = mnr;
+          red[wid * 4 + 3] = mxr;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 1; w < nwarps; ++w) {
+            mnl = umin64(mnl, red[w * 4 + 0]);
+            mxl = umax64(mxl, red[w * 4 + 1]);
+            mnr = umin64(mnr, red[w * 4 + 2]);
+            mxr = umax64(mxr, red[w * 4 + 3]);
+          }
+          finish(i, st, cnt, fl, sp, thr, nl, mnl, mxl, mnr, mxr);
+        }
+        __syncthreads();
       }
       if (tid == 0) {
         a.sub_cnt[static_cast<std::uint64_t>(r) * kSubLevels + lv] = static_cast<std::uint32_t>(nc);
@@ -1263,11 +1337,6 @@ __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
       cb ^= 1;
       nc = 2 * nint;
       if (nc > NM) __trap();  // unreachable for leaf >= 4
-      {
-        std::uint16_t* t = seg;
-        seg = seg2;
-        seg2 = t;
-      }
     }
     // internal nodes' boxes, bottom-up: the union of their children's (dkey order, as the level loop's
     // atomics; the root's box came from the level loop)
@@ -1728,9 +1797,9 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   // bottom phase: both heuristics, leaves of >= 4 points (the per-level node arrays of a subtree are
   // sized for internal nodes of >= 5 points); GK_NO_SMALL=1 turns it off (A/B experiments)
   static const bool no_small = std::getenv("GK_NO_SMALL") != nullptr;
-  static const std::uint64_t small_max_n = std::getenv("GK_SMALL_MAX_N") ? std::strtoull(std::getenv("GK_SMALL_MAX_N"), nullptr, 10)
-                                                                         : kSmallMaxN;
-  const bool bottom = !no_small && leaf >= 4 && leaf < small_cap<D>() && n <= small_max_n;
+  static const std::uint64_t max_n = std::getenv("GK_SMALL_MAX_N") ? std::strtoull(std::getenv("GK_SMALL_MAX_N"), nullptr, 10)
+                                                                   : small_max_n<D>();
+  const bool bottom = !no_small && leaf >= 4 && leaf < small_cap<D>() && n <= max_n;
   const std::size_t need = scratch_bytes<D>(n, cap_chunks, G) + (bottom ? bottom_bytes<D>(n, leaf) : 0);
   char* base = sc.reserve(need, st);
   std::size_t used = 0;
