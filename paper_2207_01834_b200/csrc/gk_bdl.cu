@@ -474,7 +474,7 @@ struct gk_bdl {
         const int slot = static_cast<int>(t - w0);
         GK_CUDA(cudaStreamWaitEvent(bst[slot], ev_pool, 0));
         build_begin(bscratch[slot], d, static_cast<int>(leaf), heuristic, pool + offs[t], pool_n, pool_ids + offs[t],
-                    cnts[t], statics[order[t]], bst[slot], grid[slot]);
+                    cnts[t], statics[order[t]], bst[slot], grid[slot], cnts[w0]);
         tr("  build launched, points", static_cast<long long>(cnts[t]));
       }
       if (w0 == 0 && rebuild_buf) {  // the buffer tree builds on st, alongside the static trees

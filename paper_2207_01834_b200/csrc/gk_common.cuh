@@ -166,7 +166,8 @@ struct BuildScratch {
 };
 // max_grid > 0 caps the cooperative grid (concurrent builds share the co-resident capacity)
 void build_begin(BuildScratch& sc, int d, int leaf, int heuristic, const double* src, std::uint64_t src_stride,
-                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st, int max_grid = 0);
+                 const std::uint32_t* src_ids, std::uint64_t n, DevTree& out, cudaStream_t st, int max_grid = 0,
+                 std::uint64_t wave_max_n = 0);  // the largest tree built concurrently with this one
 // co-resident blocks of the BuildvEB_S kernel for dimension d (its largest cooperative grid)
 int build_capacity(int d);
 // upper bound of the device bytes one build of n points allocates (scratch + the resulting tree)
