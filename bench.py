@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the range-search / kNN-graph lines")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C4/C5 lines beside the C2 metric")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "queries"],
+                    help="N > 1: independent replicas (weak scaling, default) or one query batch split over the "
+                         "replicas (strong scaling)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time for cpu_baseline")
     return ap.parse_args()
 
@@ -253,7 +256,14 @@ def run_gpu(args):
     torch.cuda.set_device(dev)
 
     d, P, Q, k = config_inputs(args.config, args.scale)
+    nq_total = len(Q)
+    if args.shard == "queries" and world > 1:
+        # every rank holds a replica of the structure and answers its slice of the batch
+        from paper_2207_01834_b200.replicas import shard_range
+        lo, hi = shard_range(nq_total, rank, world)
+        Q = Q[lo:hi]
     nq = len(Q)
+    sharded = args.shard == "queries" and world > 1
     g = gk.BDLTree(d, device=dev.index)
 
     # ---- build (Insert_L / BuildvEB_S), device-resident input: 1 cold + 3 warm Insert_L into fresh handles
@@ -310,7 +320,7 @@ def run_gpu(args):
     torch.cuda.synchronize(dev)
     from paper_2207_01834_b200.replicas import max_over_ranks, whole_job_rate
     total_ms = max_over_ranks(sum(step_ms), device=dev)
-    value = whole_job_rate(nq * args.steps, world, total_ms / 1000.0)
+    value = (nq_total * args.steps / (total_ms / 1000.0)) if sharded else whole_job_rate(nq * args.steps, world, total_ms / 1000.0)
 
     # ---- e2e through the public host API (pinned host buffers, H2D + D2H inside the timed region)
     Qh = torch.from_numpy(Q).pin_memory().numpy()
@@ -328,7 +338,7 @@ def run_gpu(args):
         e2e_s.append(time.perf_counter() - t0)
         assert rc == 0, gk.lib().gk_last_error()
     e2e_t = max_over_ranks(sum(e2e_s), device=dev)
-    e2e = whole_job_rate(nq * len(e2e_s), world, e2e_t)
+    e2e = (nq_total * len(e2e_s) / e2e_t) if sharded else whole_job_rate(nq * len(e2e_s), world, e2e_t)
     # the same call from pageable (std::vector-like) host buffers: the reference-side binding's path
     del Qh, ids_h, d2_h
     Qp = np.array(Q, copy=True)
@@ -343,7 +353,8 @@ def run_gpu(args):
         rc = gk.lib().gk_bdl_knn(g._h, Qp.ctypes.data, nq, k, ids_p.ctypes.data, d2_p.ctypes.data)
         pg_s.append(time.perf_counter() - t0)
         assert rc == 0, gk.lib().gk_last_error()
-    e2e_pageable = whole_job_rate(nq * len(pg_s), world, max_over_ranks(sum(pg_s), device=dev))
+    pg_t = max_over_ranks(sum(pg_s), device=dev)
+    e2e_pageable = (nq_total * len(pg_s) / pg_t) if sharded else whole_job_rate(nq * len(pg_s), world, pg_t)
     del Qp, ids_p, d2_p
 
     # ---- §8f-4 consumers of the same structure (reported beside the metric, not part of it):
@@ -463,9 +474,11 @@ def run_gpu(args):
                              f"points (oracle build {build_s:.1f} s, untimed); CPU {cpu_model()}"}
         line = {
             "metric": "kNN_L queries/s", "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_desc(args.config, len(P), nq, k, d),
+            "config": dict(workload_desc(args.config, len(P), nq_total, k, d),
+                           **({"parallelism": f"query-sharded replicas x{world}"} if sharded else {})),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_source": peak_src,
                          "frac_definition": "north-star (BASELINE.json) traversal roofline, kept as the legacy "
