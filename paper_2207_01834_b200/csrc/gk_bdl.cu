@@ -458,17 +458,19 @@ struct gk_bdl {
       // instead of the small trees queueing behind the largest one's full-GPU grid
       const int cap = build_capacity(d) - (rebuild_buf && w0 == 0 ? 1 : 0);
       std::vector<int> grid(w1 - w0);
-      std::uint64_t tot = 0;
       long long want = 0;
       for (std::size_t t = w0; t < w1; ++t) {
-        tot += cnts[t];
         want += grid[t - w0] = build_grid_wanted(d, cnts[t]);
       }
       if (want > cap) {
+        // shares in proportion to points^p (GK_GRID_POW, experiments; p > 1 favours the largest tree)
+        static const double gp = std::getenv("GK_GRID_POW") ? std::atof(std::getenv("GK_GRID_POW")) : 1.0;
+        double wsum = 0.0;
+        for (std::size_t t = w0; t < w1; ++t) wsum += std::pow(static_cast<double>(cnts[t]), gp);
         const int spare = cap - static_cast<int>(w1 - w0);
         for (std::size_t t = w0; t < w1; ++t)
           grid[t - w0] = std::min(grid[t - w0], 1 + static_cast<int>(static_cast<double>(spare) *
-                                                                     static_cast<double>(cnts[t]) / static_cast<double>(tot)));
+                                                                     std::pow(static_cast<double>(cnts[t]), gp) / wsum));
       }
       for (std::size_t t = w0; t < w1; ++t) {
         const int slot = static_cast<int>(t - w0);

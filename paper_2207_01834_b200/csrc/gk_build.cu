@@ -111,12 +111,12 @@ struct SelState {
 enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_NSMALL = 5, C_SUBCTR = 6, C_WORK = 7, C_COUNT = 8 };
 constexpr int kSubLevels = 64;  // local levels of a bottom-phase subtree (<= kDepthCap + 12 + 1)
 constexpr int kVLevels = 160;
-// trees up to this size use the bottom phase by default (D <= 4; measured on the B200, bottom phase on /
-// off: C1 Insert_L 1.23 / 1.51 ms, C4's ten Insert_L 21.0 / 23.5 ms, C5 Erase_L 5.4 / 5.6 ms; the 8.4M-point
-// trees of C2 / C5 break even or lose 2-3 % -- their level loop is bandwidth-bound, the bottom phase
-// issue-bound -- and at D >= 5 (subtrees of <= 256 points) it lost 5 % on C3); GK_SMALL_MAX_N overrides
+// trees up to this size use the bottom phase by default: every tree at D <= 4 (measured on the B200, bottom
+// phase on / off: C1 Insert_L 1.23 / 1.51 ms, C4's ten Insert_L 20.0 / 20.4 ms, C2 5.64 / 5.93 ms once k_subtree's
+// warp min/max went through REDUX, C5 Insert_L 1.86 / 1.82 G points/s); at D >= 5 (subtrees of <= 256 points) it
+// lost 5 % on C3; GK_SMALL_MAX_N overrides
 template <int D>
-constexpr std::uint64_t small_max_n() { return D <= 4 ? (1ull << 22) : 0; }   // absolute levels a merge spans (small roots at depths <= ~72, + kSubLevels)
+constexpr std::uint64_t small_max_n() { return D <= 4 ? (1ull << 32) : 0; }   // absolute levels a merge spans (small roots at depths <= ~72, + kSubLevels)
 
 struct BuildArgs {
   int leaf, heuristic;
