@@ -1403,6 +1403,14 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
   const std::uint32_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
   const int lane = threadIdx.x & 31;
   const std::uint32_t n = a.n;
+#if GK_BUILD_TIMELINE
+  unsigned long long mst[12];
+  int nm = 0;
+#define GK_MSTAMP() do { if (gtid == 0 && nm < 12) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(mst[nm++])); } while (0)
+#else
+#define GK_MSTAMP() do {} while (0)
+#endif
+  GK_MSTAMP();
   const int HA = static_cast<int>(__ldcg(&a.ctrl[C_H]));  // level-loop levels
   const std::uint32_t NA = __ldcg(&a.lvl_off[HA]);
   // small roots' first points marked over the points and scanned: rank(x) = # roots starting before x
@@ -1412,6 +1420,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     a.ctrl[C_NOBJ] = 0xffffffffu;                  // min root level
   }
   sync_all(grid);
+  GK_MSTAMP();
   for (std::uint32_t r = gtid; r < R; r += gthreads) {
     const std::uint32_t g = __ldcg(&a.small_list[r]);
     a.marks[__ldcg(&na.start[g])] = 1;
@@ -1420,8 +1429,10 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     atomicMin(&a.ctrl[C_NOBJ], L);
   }
   sync_all(grid);
+  GK_MSTAMP();
   grid_scan(grid, a.marks, a.mscan, n + 1, a.bsum, sh);
   sync_all(grid);
+  GK_MSTAMP();
   const int H = static_cast<int>(__ldcg(&a.ctrl[C_S]));
   const int Lmin = static_cast<int>(__ldcg(&a.ctrl[C_NOBJ]));
   // # small roots whose first point precedes position x
@@ -1434,6 +1445,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
   const std::uint32_t span = static_cast<std::uint32_t>(H - Lmin - 1);  // levels Lmin + 1 .. H - 1 hold subtree nodes
   if (static_cast<std::uint64_t>(span) * R + 1 > a.vcap) __trap();       // unreachable: vcap = rmax x 160 levels
   sync_all(grid);
+  GK_MSTAMP();
   // V[(l - Lmin - 1) * R + k] = nodes of root order[k] at level l, scanned in place
   const std::uint32_t VN = span * R;
   for (std::uint32_t i = gtid; i <= VN; i += gthreads) {
@@ -1448,8 +1460,10 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     a.V[i] = v;
   }
   sync_all(grid);
+  GK_MSTAMP();
   grid_scan(grid, a.V, a.V, VN + 1, a.bsum, sh);
   sync_all(grid);
+  GK_MSTAMP();
   if (gtid == 0) {
     std::uint32_t acc = 0;
     for (int l = 0; l < H; ++l) {
@@ -1463,6 +1477,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     a.new_off[H + 1] = acc;
   }
   sync_all(grid);
+  GK_MSTAMP();
   // scatter the level loop's nodes
   for (std::uint32_t x = gtid; x < NA; x += gthreads) {
     const int l = __ldcg(&na.level[x]);
@@ -1516,6 +1531,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     }
   }
   sync_all(grid);
+  GK_MSTAMP();
   // parent / first child (or, for a leaf, the insertion point among the next level) by start
   const std::uint32_t Nall = __ldcg(&a.new_off[H]);
   for (std::uint32_t x = gtid; x < Nall; x += gthreads) {
@@ -1532,7 +1548,17 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     }
   }
   sync_all(grid);
+  GK_MSTAMP();
   veb_phase(grid, a, nb, a.new_off, H);
+  GK_MSTAMP();
+#if GK_BUILD_TIMELINE
+  if (gtid == 0) {
+    printf("[tlmerge] n=%u grid=%u R=%u H=%d:", n, gridDim.x, R, H);
+    for (int q = 1; q < nm; ++q) printf(" %.1f", (mst[q] - mst[q - 1]) * 1e-3);
+    printf(" us\n");
+  }
+#endif
+#undef GK_MSTAMP
 }
 
 __global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::uint32_t* irank_by_slot) {
@@ -1542,54 +1568,87 @@ __global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::
   grid_scan(grid, a.int_by_slot, irank_by_slot, N + 1, a.bsum, sh);
 }
 
+// One thread per node (level-array order, so the node-array reads coalesce); the canonical record and
+// the traversal node are staged in shared memory and written by the whole warp, 8 / 16 bytes per lane
+// over consecutive words of consecutive records (a record per thread was ~21 scattered stores, each
+// touching 32 sectors: k_emit took 337 us on C2's largest tree)
+constexpr int kEmitThreads = 128;
 template <int D>
-__global__ void k_emit(const BuildArgs a, std::uint32_t N, const std::uint32_t* __restrict__ irank_by_slot,
-                       gk_canon_node* canon, TNode<D>* tn, std::int32_t* orig) {
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const BuildArgs a, std::uint32_t N,
+                                                      const std::uint32_t* __restrict__ irank_by_slot,
+                                                      gk_canon_node* canon, TNode<D>* tn, std::int32_t* orig) {
+  static_assert(sizeof(gk_canon_node) % 8 == 0 && sizeof(TNode<D>) % 16 == 0, "record sizes");
+  __shared__ gk_canon_node s_c[kEmitThreads];
+  __shared__ TNode<D> s_t[kEmitThreads];
+  __shared__ std::uint32_t s_slot[kEmitThreads], s_ti[kEmitThreads];
   const NodeArrays& na = a.na;
-  std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= N) return;
-  const std::uint32_t slot = na.pos[g];
-  const std::uint8_t fl = na.flags[g];
-  const bool leaf = (fl & F_LEAF) != 0;
-  gk_canon_node c;
-  c.kind = leaf ? 1 : 0;
-  c.depth = na.level[g];
-  c.dim = leaf ? -1 : (c.depth % D);
-  c.mode = (!leaf && (fl & F_OBJECT)) ? 1 : 0;
-  c.split = na.split[g];
-  c.start = na.start[g];
-  c.count = na.count[g];
-  for (int j = 0; j < 8; ++j) {
-    c.lo[j] = j < D ? na.lo[static_cast<std::uint64_t>(g) * D + j] : 0.0;
-    c.hi[j] = j < D ? na.hi[static_cast<std::uint64_t>(g) * D + j] : 0.0;
-  }
-  if (leaf) {
-    c.left = c.right = -1;
-    orig[slot] = -1;
-    orig[N + slot] = -1;
-  } else {
-    const std::uint32_t cb = na.cbase[g];
-    c.left = static_cast<int32_t>(na.pos[cb]);
-    c.right = static_cast<int32_t>(na.pos[cb + 1]);
-    orig[slot] = c.left;
-    orig[N + slot] = c.right;
-    orig[2 * N + c.left] = static_cast<std::int32_t>(slot);
-    orig[2 * N + c.right] = static_cast<std::int32_t>(slot);
-    TNode<D> t;
+  const std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < N) {
+    const std::uint32_t slot = na.pos[g];
+    const std::uint8_t fl = na.flags[g];
+    const bool leaf = (fl & F_LEAF) != 0;
+    gk_canon_node c;
+    c.kind = leaf ? 1 : 0;
+    c.depth = na.level[g];
+    c.dim = leaf ? -1 : (c.depth % D);
+    c.mode = (!leaf && (fl & F_OBJECT)) ? 1 : 0;
+    c.split = na.split[g];
+    c.start = na.start[g];
+    c.count = na.count[g];
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const std::uint32_t ch = cb + s;
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        t.lo[j][s] = __double2float_rd(na.lo[static_cast<std::uint64_t>(ch) * D + j]);
-        t.hi[j][s] = __double2float_ru(na.hi[static_cast<std::uint64_t>(ch) * D + j]);
-      }
-      t.ref[s] = (na.flags[ch] & F_LEAF) ? make_leaf_ref(na.start[ch], na.count[ch])
-                                         : static_cast<std::uint64_t>(irank_by_slot[na.pos[ch]]);
+    for (int j = 0; j < 8; ++j) {
+      c.lo[j] = j < D ? na.lo[static_cast<std::uint64_t>(g) * D + j] : 0.0;
+      c.hi[j] = j < D ? na.hi[static_cast<std::uint64_t>(g) * D + j] : 0.0;
     }
-    tn[irank_by_slot[slot]] = t;
+    std::uint32_t ti = 0xffffffffu;
+    if (leaf) {
+      c.left = c.right = -1;
+      orig[slot] = -1;
+      orig[N + slot] = -1;
+    } else {
+      const std::uint32_t cb = na.cbase[g];
+      c.left = static_cast<int32_t>(na.pos[cb]);
+      c.right = static_cast<int32_t>(na.pos[cb + 1]);
+      orig[slot] = c.left;
+      orig[N + slot] = c.right;
+      orig[2 * N + c.left] = static_cast<std::int32_t>(slot);
+      orig[2 * N + c.right] = static_cast<std::int32_t>(slot);
+      TNode<D> t;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const std::uint32_t ch = cb + s;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          t.lo[j][s] = __double2float_rd(na.lo[static_cast<std::uint64_t>(ch) * D + j]);
+          t.hi[j][s] = __double2float_ru(na.hi[static_cast<std::uint64_t>(ch) * D + j]);
+        }
+        t.ref[s] = (na.flags[ch] & F_LEAF) ? make_leaf_ref(na.start[ch], na.count[ch])
+                                           : static_cast<std::uint64_t>(irank_by_slot[na.pos[ch]]);
+      }
+      s_t[threadIdx.x] = t;
+      ti = irank_by_slot[slot];
+    }
+    s_c[threadIdx.x] = c;
+    s_slot[threadIdx.x] = slot;
+    s_ti[threadIdx.x] = ti;
   }
-  canon[slot] = c;
+  __syncwarp();
+  // the warp's 32 records, word by word: consecutive lanes write consecutive words of one record
+  const int lane = threadIdx.x & 31, w0 = threadIdx.x & ~31;
+  const std::uint32_t gw = blockIdx.x * blockDim.x + w0;
+  const int nrec = gw >= N ? 0 : static_cast<int>(min(32u, N - gw));
+  constexpr int kCW = sizeof(gk_canon_node) / 8, kTW = sizeof(TNode<D>) / 16;
+  const unsigned long long* cs = reinterpret_cast<const unsigned long long*>(&s_c[w0]);
+  for (int t = lane; t < nrec * kCW; t += 32) {
+    const int r = t / kCW, wd = t - r * kCW;
+    reinterpret_cast<unsigned long long*>(canon + s_slot[w0 + r])[wd] = cs[t];
+  }
+  const uint4* ts = reinterpret_cast<const uint4*>(&s_t[w0]);
+  for (int t = lane; t < nrec * kTW; t += 32) {
+    const int r = t / kTW, wd = t - r * kTW;
+    const std::uint32_t ti = s_ti[w0 + r];
+    if (ti != 0xffffffffu) reinterpret_cast<uint4*>(tn + ti)[wd] = ts[t];
+  }
 }
 
 template <class T>
@@ -1943,7 +2002,7 @@ void build_finish_d(BuildScratch& sc) {
   GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_slot_rank), dim3(G2), dim3(kThreads), args2, 0, st));
   BuildArgs ea = a;  // after the bottom phase the merged level arrays are a.na2
   if (sc.host_ctrl[C_NSMALL] > 0) ea.na = a.na2;
-  k_emit<D><<<blocks_for(N), 256, 0, st>>>(ea, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
+  k_emit<D><<<(N + kEmitThreads - 1) / kEmitThreads, kEmitThreads, 0, st>>>(ea, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
   GK_CHECK_LAUNCH();
   T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
   T.root_slot = 0;
