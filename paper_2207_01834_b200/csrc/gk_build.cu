@@ -1791,7 +1791,8 @@ int capacity_d() {
 // cheaper with fewer blocks)
 template <int D>
 int grid_wanted_d(std::uint64_t n) {
-  return static_cast<int>(std::min<std::uint64_t>(capacity_d<D>(), std::max<std::uint64_t>(1, n / 4096)));
+  static const std::uint64_t div = std::getenv("GK_GRID_DIV") ? std::strtoull(std::getenv("GK_GRID_DIV"), nullptr, 10) : 4096;
+  return static_cast<int>(std::min<std::uint64_t>(capacity_d<D>(), std::max<std::uint64_t>(1, n / div)));
 }
 
 // device scratch of one build (every array build_begin_d carves out of it, 256-byte aligned)

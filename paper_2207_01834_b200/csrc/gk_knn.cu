@@ -50,7 +50,7 @@ __device__ __forceinline__ bool lexlt(double a, std::uint32_t ia, double b, std:
 
 // distances of the query to staged leaf points p and p+1 (p even): one 16-byte shared
 // load per coordinate serves both, two independent fp64 chains
-template <int D>
+template <int D, int ROW = GK_MAX_LEAF>
 __device__ __forceinline__ void leaf_d2_pair(const double (&q)[D], const double* sp, std::uint32_t p, double& da,
                                              double& db) {
   double2 x = reinterpret_cast<const double2*>(sp)[p >> 1];
@@ -59,7 +59,7 @@ __device__ __forceinline__ void leaf_d2_pair(const double (&q)[D], const double*
   db = __dmul_rn(tb, tb);
 #pragma unroll
   for (int j = 1; j < D; ++j) {
-    x = reinterpret_cast<const double2*>(sp + j * GK_MAX_LEAF)[p >> 1];
+    x = reinterpret_cast<const double2*>(sp + j * ROW)[p >> 1];
     ta = __dsub_rn(q[j], x.x);
     tb = __dsub_rn(q[j], x.y);
     da = __dadd_rn(da, __dmul_rn(ta, ta));
@@ -73,7 +73,7 @@ __device__ __forceinline__ void leaf_d2_pair(const double (&q)[D], const double*
 // stage leaf points [s, s + c) of one tree into a warp's shared-memory block ([D][GK_MAX_LEAF] SoA + ids):
 // lane < c copies point s + lane; cp.async (LDGSTS) moves global -> shared without a register round trip.
 // The caller brackets it with __syncwarp() and calls stage_wait() before the warp reads the block.
-template <int D>
+template <int D, int ROW = GK_MAX_LEAF>
 __device__ __forceinline__ void stage_leaf(double* sp, std::uint32_t* si, const double* __restrict__ coords,
                                            const std::uint32_t* __restrict__ ids, std::uint64_t stride, std::uint64_t s,
                                            std::uint32_t c, int lane, bool with_ids) {
@@ -81,7 +81,7 @@ __device__ __forceinline__ void stage_leaf(double* sp, std::uint32_t* si, const 
 #if GK_CPASYNC
 #pragma unroll
   for (int j = 0; j < D; ++j) {
-    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sp + j * GK_MAX_LEAF + lane));
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sp + j * ROW + lane));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(coords + j * stride + s + lane));
   }
   if (with_ids) {
@@ -90,7 +90,7 @@ __device__ __forceinline__ void stage_leaf(double* sp, std::uint32_t* si, const 
   }
 #else
 #pragma unroll
-  for (int j = 0; j < D; ++j) sp[j * GK_MAX_LEAF + lane] = coords[j * stride + s + lane];
+  for (int j = 0; j < D; ++j) sp[j * ROW + lane] = coords[j * stride + s + lane];
   if (with_ids) si[lane] = ids[s + lane];
 #endif
 }
@@ -98,6 +98,41 @@ __device__ __forceinline__ void stage_wait() {
 #if GK_CPASYNC
   asm volatile("cp.async.wait_all;" ::: "memory");
 #endif
+}
+
+// ---- TMA (bulk copy) leaf staging: one elected lane issues D + 1 cp.async.bulk copies of the aligned
+// supersets of the leaf's SoA rows (16-byte aligned start, 16-byte multiple size) that complete on the
+// warp's mbarrier; the neighbouring leaves' points inside the supersets are masked with NaN afterwards.
+// Used for trees whose layout allows it (stride a multiple of 4 points, 16-byte aligned arrays).
+#ifndef GK_TMA_LEAF
+#define GK_TMA_LEAF 0
+#endif
+constexpr int kLeafRow = GK_TMA_LEAF ? GK_MAX_LEAF + 2 : GK_MAX_LEAF;  // doubles per staged coordinate row
+constexpr int kIdRow = GK_TMA_LEAF ? GK_MAX_LEAF + 4 : GK_MAX_LEAF;    // staged ids
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
 }
 
 #ifndef GK_PAIRCHK
@@ -162,8 +197,9 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   constexpr int kWarps = warps_for<KT>();
   const int K = KT > 0 ? KT : k;  // k-buffer size (compile-time for the common k)
   __shared__ std::uint64_t s_stack[kWarps][kStack];
-  __shared__ __align__(16) double s_pts[kWarps][D * GK_MAX_LEAF];
-  __shared__ std::uint32_t s_ids[kWarps][GK_MAX_LEAF];
+  __shared__ __align__(16) double s_pts[kWarps][D * kLeafRow];
+  __shared__ __align__(16) std::uint32_t s_ids[kWarps][kIdRow];
+  __shared__ __align__(8) unsigned long long s_bar[GK_TMA_LEAF ? kWarps : 1];  // one mbarrier per warp (TMA staging)
   constexpr bool kPairMode = D >= 5;  // leaf work dominates at high D (C3: ~8x packet union)
   constexpr int kPairLanes = 10;      // <= this many needing lanes: pair-parallel leaf scan
 #ifndef GK_PAIR_SMEM_Q
@@ -191,6 +227,12 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
   unsigned long long c_nodes = 0, c_leaves = 0, c_dists = 0, c_wn = 0, c_wl = 0, c_ins = 0, c_wlp = 0, c_wev = 0;
   float mdst[kStack];
+  [[maybe_unused]] unsigned tma_phase = 0;
+  [[maybe_unused]] const unsigned bar = GK_TMA_LEAF ? static_cast<unsigned>(__cvta_generic_to_shared(&s_bar[GK_TMA_LEAF ? w : 0])) : 0u;
+  if (GK_TMA_LEAF) {
+    if (lane == 0) mbar_init(bar);
+    __syncwarp();
+  }
 
   // persistent warps: each grabs the next 32-query tile (Morton order keeps
   // concurrently processed tiles adjacent, so their trees' paths share L1/L2)
@@ -258,9 +300,10 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
     civ[i * CS] = xid;
   };
   // offer staged leaf point p (distance d2) to this lane's k-buffer
+  std::uint32_t idoff = 0;  // staged ids start this many entries before staged position 0 (TMA supersets)
   auto offer = [&](double d2, std::uint32_t p) {
     if (d2 <= kd) {  // rare: lexicographic test against the k-th, then heap replace
-      const std::uint32_t pid = s_ids[w][p];
+      const std::uint32_t pid = s_ids[w][p + idoff];
       if (d2 < kd || pid < kid) {
         if (COUNT && lane == __ffs(__activemask()) - 1) c_wev++;
         sift_down(d2, pid, K);
@@ -280,24 +323,52 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
     std::uint64_t ref = ts.t[t].root;
     bool need = active;
     int sp = 0;
+    // TMA staging needs 16-byte aligned row starts and sizes: stride a multiple of 4 points (ids), aligned arrays
+    [[maybe_unused]] const bool tma_ok =
+        GK_TMA_LEAF && (stride & 3ULL) == 0 &&
+        ((reinterpret_cast<std::uintptr_t>(coords) | reinterpret_cast<std::uintptr_t>(ids)) & 15) == 0;
     while (true) {
       if (is_leaf_ref(ref)) {
         const std::uint32_t c = leaf_count(ref);
         const std::uint64_t s = leaf_start(ref);
+        std::uint32_t pbase = 0, pcs = c;  // staged position of leaf point 0; staged positions to scan
         __syncwarp();
-        stage_leaf<D>(s_pts[w], s_ids[w], coords, ids, stride, s, c, lane, true);
-        if (lane == static_cast<int>(c) && (c & 1u))
-          s_pts[w][lane] = __longlong_as_double(0x7ff8000000000000LL);  // NaN pad: never enters the top-k
-        stage_wait();
+        if (GK_TMA_LEAF && tma_ok) {
+          const std::uint64_t sa = s & ~1ULL, ia = s & ~3ULL;
+          const std::uint32_t ca = static_cast<std::uint32_t>(((s + c + 1) & ~1ULL) - sa);  // even
+          const std::uint32_t ib = static_cast<std::uint32_t>(((s + c + 3) & ~3ULL) - ia);  // multiple of 4
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the last leaf's NaN masks vs these writes
+            mbar_expect_tx(bar, static_cast<unsigned>(D) * ca * 8u + ib * 4u);
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(s_pts[w]));
+#pragma unroll
+            for (int j = 0; j < D; ++j) bulk_g2s(dst + j * kLeafRow * 8, coords + j * stride + sa, ca * 8u, bar);
+            bulk_g2s(static_cast<unsigned>(__cvta_generic_to_shared(s_ids[w])), ids + ia, ib * 4u, bar);
+          }
+          mbar_wait(bar, tma_phase);
+          tma_phase ^= 1u;
+          // the neighbouring leaves' points inside the aligned superset: NaN in coordinate 0 never enters the top-k
+          if (lane == 0 && (s & 1ULL)) s_pts[w][0] = __longlong_as_double(0x7ff8000000000000LL);
+          if (lane == 1 && ((s + c) & 1ULL)) s_pts[w][ca - 1] = __longlong_as_double(0x7ff8000000000000LL);
+          pbase = static_cast<std::uint32_t>(s & 1ULL);
+          pcs = ca;
+          idoff = static_cast<std::uint32_t>(sa - ia);
+        } else {
+          stage_leaf<D, kLeafRow>(s_pts[w], s_ids[w], coords, ids, stride, s, c, lane, true);
+          if (lane == static_cast<int>(c) && (c & 1u))
+            s_pts[w][lane] = __longlong_as_double(0x7ff8000000000000LL);  // NaN pad: never enters the top-k
+          stage_wait();
+          if (GK_TMA_LEAF) idoff = 0;
+        }
         __syncwarp();
         const unsigned needm = __ballot_sync(0xffffffffu, need);
         const int m = __popc(needm);
         if (!kPairMode || m > kPairLanes) {
           // each lane scans all points against its own query,
           // two independent distance chains per iteration (fp64 latency)
-          for (std::uint32_t p = 0; p < c; p += 2) {
+          for (std::uint32_t p = 0; p < pcs; p += 2) {
             double da, db;
-            leaf_d2_pair<D>(q, s_pts[w], p, da, db);
+            leaf_d2_pair<D, kLeafRow>(q, s_pts[w], p, da, db);
             if (!GK_PAIRCHK || fmin(da, db) <= kd) {  // one test rejects both (the common case)
               offer(da, p);
               offer(db, p + 1);
@@ -319,23 +390,23 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
             if (kSmemQ) {
               if (valid) {
                 const double* qo = &s_q[w][own];
-                const double t = __dsub_rn(qo[0], s_pts[w][pp]);
+                const double t = __dsub_rn(qo[0], s_pts[w][pp + pbase]);
                 d2 = __dmul_rn(t, t);
 #pragma unroll
                 for (int j = 1; j < D; ++j) {
-                  const double tt = __dsub_rn(qo[j * 32], s_pts[w][j * GK_MAX_LEAF + pp]);
+                  const double tt = __dsub_rn(qo[j * 32], s_pts[w][j * kLeafRow + pp + pbase]);
                   d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
                 }
               }
             } else {
               // the owner's query straight from its registers (keeps ~14 KB of shared memory per
               // block free at D = 7: 4 blocks per SM instead of 3)
-              const std::uint32_t ppc = valid ? pp : 0u;
+              const std::uint32_t ppc = (valid ? pp : 0u) + pbase;
               const double t = __dsub_rn(__shfl_sync(0xffffffffu, q[0], own), s_pts[w][ppc]);
               d2 = __dmul_rn(t, t);
 #pragma unroll
               for (int j = 1; j < D; ++j) {
-                const double tt = __dsub_rn(__shfl_sync(0xffffffffu, q[j], own), s_pts[w][j * GK_MAX_LEAF + ppc]);
+                const double tt = __dsub_rn(__shfl_sync(0xffffffffu, q[j], own), s_pts[w][j * kLeafRow + ppc]);
                 d2 = __dadd_rn(d2, __dmul_rn(tt, tt));
               }
             }
@@ -347,7 +418,7 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
               const int ob = __shfl_sync(0xffffffffu, own, b);
               const double db = __shfl_sync(0xffffffffu, d2, b);
               const std::uint32_t pb = __shfl_sync(0xffffffffu, pp, b);
-              if (lane == ob) offer(db, pb);
+              if (lane == ob) offer(db, pb + pbase);
             }
             __syncwarp();
             pp += dp;
