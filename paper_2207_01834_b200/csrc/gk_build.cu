@@ -108,7 +108,7 @@ struct SelState {
 };
 
 // control words (device)
-enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_NSMALL = 5, C_SUBCTR = 6, C_WORK = 7, C_COUNT = 8 };
+enum Ctrl { C_S = 0, C_NOBJ = 1, C_H = 2, C_N = 3, C_LEVEL = 4, C_NSMALL = 5, C_SUBCTR = 6, C_WORK = 7, C_NCHUNKS = 8, C_COUNT = 9 };
 constexpr int kSubLevels = 64;  // local levels of a bottom-phase subtree (<= kDepthCap + 12 + 1)
 constexpr int kVLevels = 160;
 // trees up to this size use the bottom phase by default: every tree at D <= 4 (measured on the B200, bottom
@@ -132,11 +132,14 @@ struct BuildArgs {
   NodeArrays na;
   std::uint32_t* lvl_off;   // [kMaxLevels + 2]
   std::uint32_t* ctrl;      // [C_COUNT]
-  std::uint32_t *chunk_cnt, *chunk_off, *chunk_node, *chunk_left, *left_scan, *is_int, *irank, *obj_list;
+  // chunk_off / chunk_node: a level's chunk offsets per node and chunk -> node map, ping-pong by level parity
+  // (the parent level's F writes them while its G still reads its own); ccnt / coff: chunks of a node's
+  // children and their exclusive scan
+  std::uint32_t *chunk_off[2], *chunk_node[2], *ccnt, *coff, *chunk_left, *left_scan, *is_int, *irank, *obj_list;
   unsigned long long* keys;
   SelState* sel;
   std::uint32_t* hist;      // [kSelCap * 256]
-  std::uint32_t* bsum;      // [gridDim]
+  std::uint32_t* bsum;      // [3 * gridDim + 2]
   std::uint32_t* int_by_slot;  // [cap + 1]
   // bottom phase (k_subtree + k_merge): subtrees of nodes with leaf < count <= Tsmall, one block each
   std::uint32_t Tsmall;        // 0: off (object-median heuristic, leaf < 4, or a tree that fits no block)
@@ -305,7 +308,10 @@ __device__ void veb_phase(cg::grid_group& grid, const BuildArgs& a, const NodeAr
 // not cost the dense levels registers.  PH = 1 resumes at ctrl[C_LEVEL] (or returns at once when
 // PH = 0 finished the whole build) and runs the remaining levels and the vEB phase.
 template <int D, int PH>
-__global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_build(const BuildArgs a) {
+#ifndef GK_BUILD_MINB_HI
+#define GK_BUILD_MINB_HI 0  // D >= 5: min blocks per SM for ptxas (0: none)
+#endif
+__global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : GK_BUILD_MINB_HI)) k_build(const BuildArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ std::uint32_t sh[32];
   const NodeArrays& na = a.na;
@@ -355,8 +361,9 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     a.lvl_off[0] = 0;
     a.ctrl[C_S] = 1;
     a.ctrl[C_NOBJ] = 0;
-    a.chunk_cnt[0] = (n + kc - 1) / kc;  // deeper levels' chunk counts are written by F
-    a.chunk_cnt[1] = 0;
+    a.chunk_off[0][0] = 0;  // the root's chunks (deeper levels' offsets and maps are written by the parent level's F)
+    a.chunk_off[0][1] = (n + kc - 1) / kc;
+    a.ctrl[C_NCHUNKS] = (n + kc - 1) / kc;
     a.ctrl[C_LEVEL] = 0xffffffffu;
     a.ctrl[C_NSMALL] = 0;
     a.ctrl[C_SUBCTR] = 0;
@@ -367,7 +374,10 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       a.keys[j * 2 + 1] = 0ULL;
     }
   }
-  if (PH == 0) sync_all(grid);
+  if (PH == 0) {
+    for (std::uint32_t c = gtid; c < (n + kc - 1) / kc; c += gthreads) a.chunk_node[0][c] = 0;
+    sync_all(grid);
+  }
   [[maybe_unused]] const int level0 = level;
 #if GK_BUILD_TIMELINE
   unsigned long long tl_st[33][5];
@@ -387,25 +397,20 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     const bool box_pass = level == 0 || !kChildBoxes;  // else the parent's G accumulated the boxes
     const bool spatial_level = a.heuristic != GK_OBJECT_MEDIAN && level < kDepthCap;
 
-    // chunk offsets; with many nodes (one or two chunks each) the scan also writes the
-    // chunk -> node map, with few nodes a warp per node writes it
-    const bool fused_map = S >= nwarps;
-    grid_scan(grid, a.chunk_cnt, a.chunk_off, S + 1, a.bsum, sh, fused_map ? a.chunk_node : nullptr);
-    sync_all(grid);
+    // this level's chunk offsets and chunk -> node map: written by the parent level's F (level 0: at
+    // the start), so a level costs four grid barriers: C+D | E + scan partials | scan finish | F+G
+    const std::uint32_t* chunk_off = a.chunk_off[level & 1];
+    const std::uint32_t* chunk_node = a.chunk_node[level & 1];
+    std::uint32_t* chunk_off_nx = a.chunk_off[(level & 1) ^ 1];
+    std::uint32_t* chunk_node_nx = a.chunk_node[(level & 1) ^ 1];
     GK_PHASE_STAMP(1);
-    const std::uint32_t nchunks = __ldcg(&a.chunk_off[S]);
+    const std::uint32_t nchunks = __ldcg(&a.ctrl[C_NCHUNKS]);
     // Sparse levels (many small chunks per warp): the partition runs in lane groups (PH = 1)
     const std::uint32_t cpw = nchunks / nwarps;
     if (PH == 0 && kGroupedSparse && cpw >= kGroup16Chunks) {
-      if (gtid == 0) a.ctrl[C_LEVEL] = static_cast<std::uint32_t>(level);  // PH = 1 redoes this level's scan
+      if (gtid == 0) a.ctrl[C_LEVEL] = static_cast<std::uint32_t>(level);  // PH = 1 resumes here
       GK_TL_PRINT(level0);
       return;
-    }
-    if (!fused_map) {
-      for (std::uint32_t v = gwarp; v < S; v += nwarps) {
-        const std::uint32_t c0 = __ldcg(&a.chunk_off[v]), c1 = __ldcg(&a.chunk_off[v + 1]);
-        for (std::uint32_t c = c0 + lane; c < c1; c += 32) a.chunk_node[c] = v;
-      }
     }
 
     // C: node records and split decisions (needs the final boxes)
@@ -443,23 +448,32 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     };
 
     if (box_pass) {
-      if (!fused_map) sync_all(grid);  // B reads the chunk map
       // B: per chunk: bounding box
       for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
-        const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+        const std::uint32_t v = __ldcg(&chunk_node[c]), g = off + v;
         const std::uint32_t s0 = __ldcg(&na.start[g]), cnt = __ldcg(&na.count[g]);
-        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+        const std::uint32_t first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
         const std::uint32_t end = min(first + kc, s0 + cnt);
         double mn[D], mx[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) { mn[j] = __longlong_as_double(0x7ff0000000000000LL); mx[j] = -mn[j]; }
-        for (std::uint32_t i = first + lane; i < end; i += 32) {
+        constexpr int UB = 2;  // rounds whose loads are in flight together (the pass is latency-bound)
+        for (std::uint32_t i0 = first + lane; i0 < end; i0 += 32 * UB) {
+          double x[UB][D];
 #pragma unroll
-          for (int j = 0; j < D; ++j) {
-            const double x = __ldcg(&cur[j * cur_stride + i]);
-            mn[j] = fmin(mn[j], x);
-            mx[j] = fmax(mx[j], x);
+          for (int u = 0; u < UB; ++u) {
+            const std::uint32_t i = i0 + 32 * u;
+#pragma unroll
+            for (int j = 0; j < D; ++j)  // NaN past the end: fmin / fmax keep the other operand
+              x[u][j] = i < end ? __ldcg(&cur[j * cur_stride + i]) : __longlong_as_double(0x7ff8000000000000LL);
           }
+#pragma unroll
+          for (int u = 0; u < UB; ++u)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              mn[j] = fmin(mn[j], x[u][j]);
+              mx[j] = fmax(mx[j], x[u][j]);
+            }
         }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -483,7 +497,6 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       node_records();
     } else {
       node_records();
-      if (!fused_map) sync_all(grid);  // D reads the chunk map
     }
 
     // Sparse levels (>= 64 chunks per warp, chunks of a few dozen points): the count pass runs
@@ -495,11 +508,11 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     if (lane_mode) {
       for (std::uint32_t c = gwarp * 32 + lane; c < ((nchunks + 31) & ~31u); c += nwarps * 32) {
         if (c >= nchunks) continue;
-        const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+        const std::uint32_t v = __ldcg(&chunk_node[c]), g = off + v;
         const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
         std::uint32_t cnt = 0;
         if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf) && nn > a.Tsmall) {
-          const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+          const std::uint32_t first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
           const std::uint32_t end = min(first + kc, s0 + nn);
           const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
           const double h = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2 + 1]));
@@ -513,11 +526,11 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       }
     } else
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
-      const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+      const std::uint32_t v = __ldcg(&chunk_node[c]), g = off + v;
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
       std::uint32_t cnt = 0;
       if (spatial_level && nn > static_cast<std::uint32_t>(a.leaf) && nn > a.Tsmall) {
-        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+        const std::uint32_t first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
         const std::uint32_t end = min(first + kc, s0 + nn);
         const double l = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2]));
         const double h = dkey_inv(__ldcg(&a.keys[(static_cast<std::uint64_t>(v) * D + cdim) * 2 + 1]));
@@ -544,7 +557,11 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
 
     // E: degenerate spatial splits -> object median; internal flags; reset the next
     // level's box accumulators (this level's were consumed by C and D)
-    for (std::uint32_t v = gtid; v <= S; v += gthreads) {
+    // (each block on its own scan segment of [0, S], so that the scans' block sums follow after a block barrier)
+    const std::uint32_t e_seg = (S + 1 + gridDim.x - 1) / gridDim.x;
+    const std::uint32_t e_lo = min(S + 1, blockIdx.x * e_seg), e_hi = min(S + 1, e_lo + e_seg);
+    for (std::uint32_t v = e_lo + threadIdx.x; v < e_hi; v += blockDim.x) {
+      a.ccnt[v] = 0;
       if (v == S) { a.is_int[S] = 0; continue; }
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
@@ -566,17 +583,24 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       }
       a.is_int[v] = 1;
       const std::uint32_t cnt = __ldcg(&na.count[g]);
+      std::uint32_t nl = __ldcg(&na.nleft[g]);
       if (!(fl & F_OBJECT)) {
-        const std::uint32_t nl = __ldcg(&na.nleft[g]);
         if (nl == 0 || nl == cnt) { fl |= F_OBJECT; na.flags[g] = fl; }
       }
       if (fl & F_OBJECT) {
         const std::uint32_t o = atomicAdd(&a.ctrl[C_NOBJ], 1u);
         a.obj_list[o] = g;
-        na.nleft[g] = cnt / 2;
+        nl = cnt / 2;
+        na.nleft[g] = nl;
         na.pos[g] = o;  // temporary: object index (pos is recomputed by the vEB phase)
       }
+      a.ccnt[v] = (nl + kc - 1) / kc + (cnt - nl + kc - 1) / kc;  // the children's chunks
     }
+    __syncthreads();
+    // block sums of the three scans: BFS child slots, the children's chunk offsets, chunk left counts
+    scan_partial(a.is_int, S + 1, a.bsum, sh);
+    scan_partial(a.ccnt, S + 1, a.bsum + 2 * gridDim.x, sh);
+    scan_partial(a.chunk_left, nchunks + 1, a.bsum + gridDim.x, sh);
     sync_all(grid);
     GK_PHASE_STAMP(3);
 
@@ -593,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       sync_all(grid);
       for (int p = 0; p < 12; ++p) {
         for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
-          const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+          const std::uint32_t v = __ldcg(&chunk_node[c]), g = off + v;
           if ((__ldcg(&na.flags[g]) & (F_LEAF | F_OBJECT)) != F_OBJECT) continue;
           const std::uint32_t o = __ldcg(&na.pos[g]);
           if (o < b0 || o >= b0 + nb) continue;
@@ -601,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
           s.hi = __ldcg(&a.sel[o - b0].hi);
           s.lo = __ldcg(&a.sel[o - b0].lo);
           const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
-          const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+          const std::uint32_t first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
           const std::uint32_t end = min(first + kc, s0 + nn);
           for (std::uint32_t i0 = first; i0 < end; i0 += 32) {
             const std::uint32_t i = i0 + lane;
@@ -655,10 +679,10 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
     }
     if (nobj) {  // left counts of object nodes ((x_c, id) < threshold)
       for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
-        const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+        const std::uint32_t v = __ldcg(&chunk_node[c]), g = off + v;
         if ((__ldcg(&na.flags[g]) & (F_LEAF | F_OBJECT)) != F_OBJECT) continue;
         const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
-        const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+        const std::uint32_t first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
         const std::uint32_t end = min(first + kc, s0 + nn);
         const double s = __ldcg(&na.split[g]);
         const std::uint32_t tid = __ldcg(&na.thr_id[g]);
@@ -675,37 +699,57 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
         if (lane == 0) a.chunk_left[c] = cnt;
       }
       sync_all(grid);
+      scan_partial(a.chunk_left, nchunks + 1, a.bsum + gridDim.x, sh);  // again, with the object nodes' counts
+      sync_all(grid);
     }
 
-    // scans (one shared barrier): BFS child slots (internal ranks) and chunk left-count offsets
-    scan_partial(a.is_int, S + 1, a.bsum, sh);
-    scan_partial(a.chunk_left, nchunks + 1, a.bsum + gridDim.x, sh);
-    sync_all(grid);
     scan_finish(a.is_int, a.irank, S + 1, a.bsum, sh);
+    scan_finish(a.ccnt, a.coff, S + 1, a.bsum + 2 * gridDim.x, sh);
     scan_finish(a.chunk_left, a.left_scan, nchunks + 1, a.bsum + gridDim.x, sh);
     sync_all(grid);
     GK_PHASE_STAMP(4);
     const std::uint32_t nint = __ldcg(&a.irank[S]);
+    const std::uint32_t nchunks_nx = __ldcg(&a.coff[S]);
     const std::uint32_t next_off = off + S;
 
-    // F: child node records; G: stable partition
-    for (std::uint32_t v = gtid; v < S; v += gthreads) {
-      const std::uint32_t g = off + v;
-      const std::uint32_t cb = next_off + 2 * __ldcg(&a.irank[v]);
-      na.cbase[g] = cb;
-      if (__ldcg(&na.flags[g]) & (F_LEAF | F_SMALL)) continue;
-      const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]), nl = __ldcg(&na.nleft[g]);
-      na.start[cb] = s0; na.count[cb] = nl; na.parent[cb] = g;
-      na.start[cb + 1] = s0 + nl; na.count[cb + 1] = nn - nl; na.parent[cb + 1] = g;
-      na.nleft[cb] = 0;
-      na.nleft[cb + 1] = 0;
-      // the next level's chunk counts (its first scan input)
-      const std::uint32_t u = cb - next_off;
-      a.chunk_cnt[u] = (nl + kc - 1) / kc;
-      a.chunk_cnt[u + 1] = (nn - nl + kc - 1) / kc;
+    // F: child node records, the next level's chunk offsets and chunk -> node map (a node's few entries by
+    // its own thread, a node of many chunks by its whole warp); G: stable partition
+    for (std::uint32_t vb = gwarp * 32; vb < S; vb += nwarps * 32) {
+      const std::uint32_t v = vb + lane, g = off + v;
+      std::uint32_t u = 0, c0 = 0, c1 = 0, c2 = 0;
+      if (v < S) {
+        const std::uint32_t cb = next_off + 2 * __ldcg(&a.irank[v]);
+        na.cbase[g] = cb;
+        if (!(__ldcg(&na.flags[g]) & (F_LEAF | F_SMALL))) {
+          const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]), nl = __ldcg(&na.nleft[g]);
+          na.start[cb] = s0; na.count[cb] = nl; na.parent[cb] = g;
+          na.start[cb + 1] = s0 + nl; na.count[cb + 1] = nn - nl; na.parent[cb + 1] = g;
+          na.nleft[cb] = 0;
+          na.nleft[cb + 1] = 0;
+          u = cb - next_off;
+          c0 = __ldcg(&a.coff[v]);
+          c1 = c0 + (nl + kc - 1) / kc;
+          c2 = c1 + (nn - nl + kc - 1) / kc;
+          chunk_off_nx[u] = c0;
+          chunk_off_nx[u + 1] = c1;
+        }
+      }
+      const bool wide = c2 - c0 > 8;
+      if (!wide) {
+        for (std::uint32_t c = c0; c < c2; ++c) chunk_node_nx[c] = c < c1 ? u : u + 1;
+      }
+      unsigned wm = __ballot_sync(0xffffffffu, wide);
+      while (wm) {
+        const int src = __ffs(wm) - 1;
+        wm &= wm - 1;
+        const std::uint32_t bu = __shfl_sync(0xffffffffu, u, src), b0 = __shfl_sync(0xffffffffu, c0, src),
+                            b1 = __shfl_sync(0xffffffffu, c1, src), b2 = __shfl_sync(0xffffffffu, c2, src);
+        for (std::uint32_t c = b0 + lane; c < b2; c += 32) chunk_node_nx[c] = c < b1 ? bu : bu + 1;
+      }
     }
     if (gtid == 0) {
-      a.chunk_cnt[2 * nint] = 0;
+      chunk_off_nx[2 * nint] = nchunks_nx;
+      a.ctrl[C_NCHUNKS] = nchunks_nx;
       a.ctrl[C_NOBJ] = 0;
     }
     // Sparse levels (many small chunks per warp): the warp splits into 32/gl lane groups that
@@ -723,12 +767,12 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
         std::uint32_t v = 0, g = 0, s0 = 0, first = 0, end = 0;
         std::uint8_t fl = F_LEAF;
         if (c < nchunks) {
-          v = __ldcg(&a.chunk_node[c]);
+          v = __ldcg(&chunk_node[c]);
           g = off + v;
           fl = __ldcg(&na.flags[g]);
           s0 = __ldcg(&na.start[g]);
           const std::uint32_t nn = __ldcg(&na.count[g]);
-          first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+          first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
           end = min(first + kc, s0 + nn);
         }
         const bool part = !(fl & (F_LEAF | F_SMALL));
@@ -746,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
           s = __ldcg(&na.split[g]);
           tid = obj ? __ldcg(&na.thr_id[g]) : 0u;
           nl = __ldcg(&na.nleft[g]);
-          lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&a.chunk_off[v])]);
+          lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&chunk_off[v])]);
         }
         const std::uint32_t lb0 = lbefore;
         double mnl[D], mxl[D], mnr[D], mxr[D];
@@ -816,10 +860,10 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       }
     } else
     for (std::uint32_t c = gwarp; c < nchunks; c += nwarps) {
-      const std::uint32_t v = __ldcg(&a.chunk_node[c]), g = off + v;
+      const std::uint32_t v = __ldcg(&chunk_node[c]), g = off + v;
       const std::uint8_t fl = __ldcg(&na.flags[g]);
       const std::uint32_t s0 = __ldcg(&na.start[g]), nn = __ldcg(&na.count[g]);
-      const std::uint32_t first = s0 + (c - __ldcg(&a.chunk_off[v])) * kc;
+      const std::uint32_t first = s0 + (c - __ldcg(&chunk_off[v])) * kc;
       const std::uint32_t end = min(first + kc, s0 + nn);
       if (fl & (F_LEAF | F_SMALL)) {  // finished (a small root's subtree is built by the bottom phase)
         for (std::uint32_t i = first + lane; i < end; i += 32) {
@@ -833,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : 0)) k_buil
       const double s = __ldcg(&na.split[g]);
       const std::uint32_t tid = obj ? __ldcg(&na.thr_id[g]) : 0u;
       const std::uint32_t nl = __ldcg(&na.nleft[g]);
-      std::uint32_t lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&a.chunk_off[v])]);
+      std::uint32_t lbefore = __ldcg(&a.left_scan[c]) - __ldcg(&a.left_scan[__ldcg(&chunk_off[v])]);
       const std::uint32_t lb0 = lbefore;
       // the children's bounding boxes, accumulated while partitioning (the next level needs no box pass)
       double mnl[D], mxl[D], mnr[D], mxr[D];
@@ -1799,9 +1843,9 @@ int grid_wanted_d(std::uint64_t n) {
 template <int D>
 std::size_t scratch_bytes(std::uint64_t n, std::uint64_t cap_chunks, int G) {
   const std::uint64_t cap = 2 * n - 1, cap_level = std::min<std::uint64_t>(cap, n);
-  return 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) + (cap_level + 1) * 4 * 5 +
-         cap_chunks * 4 * 3 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 + C_COUNT * 4 + kSelCap * sizeof(SelState) +
-         kSelCap * 256 * 4 + (2 * G + 2) * 4 + 4 * (cap + 1) + 40 * 256;
+  return 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) + (cap_level + 1) * 4 * 7 +
+         cap_chunks * 4 * 4 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 + C_COUNT * 4 + kSelCap * sizeof(SelState) +
+         kSelCap * 256 * 4 + (3 * G + 2) * 4 + 4 * (cap + 1) + 44 * 256;
 }
 
 // the bottom phase's arrays (small roots, subtree node records, merge scratch, merged level arrays)
@@ -1898,18 +1942,21 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   na.hi = reinterpret_cast<double*>(take(cap * D * 8));
   a.lvl_off = reinterpret_cast<std::uint32_t*>(take((kMaxLevels + 2) * 4));
   a.ctrl = reinterpret_cast<std::uint32_t*>(take(C_COUNT * 4));
-  a.chunk_cnt = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
-  a.chunk_off = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.chunk_off[0] = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.chunk_off[1] = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.ccnt = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
+  a.coff = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
   a.is_int = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
   a.irank = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
   a.obj_list = reinterpret_cast<std::uint32_t*>(take((cap_level + 1) * 4));
-  a.chunk_node = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
+  a.chunk_node[0] = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
+  a.chunk_node[1] = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
   a.chunk_left = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
   a.left_scan = reinterpret_cast<std::uint32_t*>(take(cap_chunks * 4));
   a.keys = reinterpret_cast<unsigned long long*>(take(cap_level * D * 2 * 8));
   a.sel = reinterpret_cast<SelState*>(take(kSelCap * sizeof(SelState)));
   a.hist = reinterpret_cast<std::uint32_t*>(take(kSelCap * 256 * 4));
-  a.bsum = reinterpret_cast<std::uint32_t*>(take((2 * G + 2) * 4));
+  a.bsum = reinterpret_cast<std::uint32_t*>(take((3 * G + 2) * 4));
   a.int_by_slot = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
   a.Tsmall = bottom ? static_cast<std::uint32_t>(small_cap<D>()) : 0u;
   if (bottom) {

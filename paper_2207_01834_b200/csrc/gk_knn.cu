@@ -135,6 +135,9 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
       : "memory");
 }
 
+#ifndef GK_PF_CHILD
+#define GK_PF_CHILD 0  // 1: L1 prefetch of both children's node records at a node visit; 2: also leaf children's rows
+#endif
 #ifndef GK_PAIRCHK
 #define GK_PAIRCHK 0  // 1: one min(da, db) <= kd test in front of the pair's two offers
 #endif
@@ -446,6 +449,20 @@ __global__ void __launch_bounds__(warps_for<KT>() * 32, (D <= 4 ? 5 : 4)) k_knn(
           if (need) c_nodes++;
           c_wn++;
         }
+#if GK_PF_CHILD
+        // both children's records (or leaf rows) start towards L1 while this node's boxes are tested
+        {
+          const std::uint64_t r0 = rr.x, r1 = rr.y;
+          if (!is_leaf_ref(r0)) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + r0 * (D + 1)));
+          else if (GK_PF_CHILD >= 2 && lane <= D)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(lane < D ? static_cast<const void*>(coords + lane * stride + leaf_start(r0))
+                                                                  : static_cast<const void*>(ids + leaf_start(r0))));
+          if (!is_leaf_ref(r1)) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + r1 * (D + 1)));
+          else if (GK_PF_CHILD >= 2 && lane <= D)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(lane < D ? static_cast<const void*>(coords + lane * stride + leaf_start(r1))
+                                                                  : static_cast<const void*>(ids + leaf_start(r1))));
+        }
+#endif
         float m0, m1;
         box_lb_pair<D>(qlo2, qhi2, u, u + D, m0, m1);
         const bool w0 = m0 <= kthf, w1 = m1 <= kthf;
