@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "gk_common.cuh"
@@ -1023,7 +1024,8 @@ __host__ __device__ constexpr std::size_t small_smem() {
 
 // in-place exclusive scan of a[0, n) (a[n] = total) by the whole block; wsum: 32 words of shared memory
 __device__ void block_exscan_u16(std::uint16_t* a, int n, std::uint32_t* wsum) {
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  constexpr int nth = kSubThreads, nw = nth >> 5;  // compile-time: no integer division for the segment size
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int per = (n + nth - 1) / nth;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   std::uint32_t s = 0;
@@ -1100,7 +1102,8 @@ __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
   std::uint16_t* bigl = nscan + NM + 1;                                                // [T / kSubBig + 1]
 
   const NodeArrays& na = a.na;
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarps = nth >> 5;
+  constexpr int nth = kSubThreads, nwarps = nth >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const std::uint64_t N = a.n;  // SoA stride of the output
   const bool spatial_heur = a.heuristic != GK_OBJECT_MEDIAN;
@@ -1211,81 +1214,87 @@ __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
           }
           continue;
         }
-        const int nit = (cnt + 31) >> 5;
-        bool v[4];
-        int ip[4];
-        double x[4];
-        unsigned b[4];
+        // rounds of 32 points, compiled for 1, 2 and 4 rounds (most nodes of the bottom levels hold <= 64 points)
+        auto split_node = [&](auto nit_c) {
+          constexpr int NIT = decltype(nit_c)::value;
+          bool v[NIT];
+          int ip[NIT];
+          double x[NIT];
+          unsigned b[NIT];
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int q = 32 * it + lane;
-          v[it] = it < nit && q < cnt;
-          ip[it] = v[it] ? perm[st + q] : 0;
-          x[it] = v[it] ? X[c * T + ip[it]] : 0.0;
-          b[it] = 0;
-        }
-        std::uint8_t fl = F_OBJECT;
-        double sp = 0.0;
-        std::uint32_t thr = 0;
-        int nl = 0;
-        if (spatial) {
-          sp = __dmul_rn(__dadd_rn(dkey_inv(cbl[i]), dkey_inv(cbh[i])), 0.5);  // (lo + hi) / 2 exactly
-#pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            b[it] = __ballot_sync(0xffffffffu, v[it] && x[it] < sp);
-            nl += __popc(b[it]);
+          for (int it = 0; it < NIT; ++it) {
+            const int q = 32 * it + lane;
+            v[it] = q < cnt;
+            ip[it] = v[it] ? perm[st + q] : 0;
+            x[it] = v[it] ? X[c * T + ip[it]] : 0.0;
+            b[it] = 0;
           }
-          if (nl > 0 && nl < cnt) fl = 0;
-        }
-        if (fl == F_OBJECT) {  // object median: the key of rank floor(cnt/2) in (x_c, id) order (-0 == +0)
-          const int m = cnt / 2;
-          std::uint32_t idv[4];
+          std::uint8_t fl = F_OBJECT;
+          double sp = 0.0;
+          std::uint32_t thr = 0;
+          int nl = 0;
+          if (spatial) {
+            sp = __dmul_rn(__dadd_rn(dkey_inv(cbl[i]), dkey_inv(cbh[i])), 0.5);  // (lo + hi) / 2 exactly
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            idv[it] = v[it] ? ID[ip[it]] : 0u;
-            int rank = -1;
-            if (v[it]) {
-              rank = 0;
-              for (int q = st; q < st + cnt; ++q) {
-                const int iq = perm[q];
-                const double xq = X[c * T + iq];
-                rank += (xq < x[it] || (xq == x[it] && ID[iq] < idv[it])) ? 1 : 0;
+            for (int it = 0; it < NIT; ++it) {
+              b[it] = __ballot_sync(0xffffffffu, v[it] && x[it] < sp);
+              nl += __popc(b[it]);
+            }
+            if (nl > 0 && nl < cnt) fl = 0;
+          }
+          if (fl == F_OBJECT) {  // object median: the key of rank floor(cnt/2) in (x_c, id) order (-0 == +0)
+            const int m = cnt / 2;
+            std::uint32_t idv[NIT];
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+              idv[it] = v[it] ? ID[ip[it]] : 0u;
+              int rank = -1;
+              if (v[it]) {
+                rank = 0;
+                for (int q = st; q < st + cnt; ++q) {
+                  const int iq = perm[q];
+                  const double xq = X[c * T + iq];
+                  rank += (xq < x[it] || (xq == x[it] && ID[iq] < idv[it])) ? 1 : 0;
+                }
+              }
+              const unsigned hit = __ballot_sync(0xffffffffu, rank == m);
+              if (hit) {
+                const int src = __ffs(hit) - 1;
+                sp = __dadd_rn(__shfl_sync(0xffffffffu, x[it], src), 0.0);  // canonical +0, as the level loop
+                thr = __shfl_sync(0xffffffffu, idv[it], src);
               }
             }
-            const unsigned hit = __ballot_sync(0xffffffffu, rank == m);
-            if (hit) {
-              const int src = __ffs(hit) - 1;
-              sp = __dadd_rn(__shfl_sync(0xffffffffu, x[it], src), 0.0);  // canonical +0, as the level loop
-              thr = __shfl_sync(0xffffffffu, idv[it], src);
+            nl = 0;
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+              b[it] = __ballot_sync(0xffffffffu, v[it] && (x[it] < sp || (x[it] == sp && idv[it] < thr)));
+              nl += __popc(b[it]);
             }
           }
-          nl = 0;
+          // stable partition + the children's boxes in the next level's split dimension
+          unsigned long long mnl = ~0ULL, mxl = 0ULL, mnr = ~0ULL, mxr = 0ULL;
+          int before = 0;
 #pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            b[it] = __ballot_sync(0xffffffffu, v[it] && (x[it] < sp || (x[it] == sp && idv[it] < thr)));
-            nl += __popc(b[it]);
+          for (int it = 0; it < NIT; ++it) {
+            const bool pr = (b[it] >> lane) & 1u;
+            if (v[it]) {
+              const int q = 32 * it + lane;
+              const int rk = before + __popc(b[it] & lt_mask);
+              const int np = pr ? st + rk : st + nl + (q - rk);
+              perm2[np] = static_cast<std::uint16_t>(ip[it]);
+              const unsigned long long k = dkey(X[c1 * T + ip[it]]);
+              if (pr) { mnl = umin64(mnl, k); mxl = umax64(mxl, k); }
+              else { mnr = umin64(mnr, k); mxr = umax64(mxr, k); }
+            }
+            before += __popc(b[it]);
           }
-        }
-        // stable partition + the children's boxes in the next level's split dimension
-        unsigned long long mnl = ~0ULL, mxl = 0ULL, mnr = ~0ULL, mxr = 0ULL;
-        int before = 0;
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const bool pr = (b[it] >> lane) & 1u;
-          if (v[it]) {
-            const int q = 32 * it + lane;
-            const int rk = before + __popc(b[it] & lt_mask);
-            const int np = pr ? st + rk : st + nl + (q - rk);
-            perm2[np] = static_cast<std::uint16_t>(ip[it]);
-            const unsigned long long k = dkey(X[c1 * T + ip[it]]);
-            if (pr) { mnl = umin64(mnl, k); mxl = umax64(mxl, k); }
-            else { mnr = umin64(mnr, k); mxr = umax64(mxr, k); }
-          }
-          before += __popc(b[it]);
-        }
-        warp_minmax(mnl, mxl);
-        warp_minmax(mnr, mxr);
-        if (lane == 0) finish(i, st, cnt, fl, sp, thr, nl, mnl, mxl, mnr, mxr);
+          warp_minmax(mnl, mxl);
+          warp_minmax(mnr, mxr);
+          if (lane == 0) finish(i, st, cnt, fl, sp, thr, nl, mnl, mxl, mnr, mxr);
+        };
+        if (cnt <= 32) split_node(std::integral_constant<int, 1>{});
+        else if (cnt <= 64) split_node(std::integral_constant<int, 2>{});
+        else split_node(std::integral_constant<int, 4>{});
       }
       // ---- block mode: nodes of more than kSubBig points, the whole block on one node at a time
       for (int bi = 0; bi < nbig; ++bi) {
