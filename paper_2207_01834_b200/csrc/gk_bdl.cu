@@ -137,7 +137,7 @@ __global__ void k_bloom_build(const double* __restrict__ coords, std::uint64_t n
   const std::uint64_t key = bloom_key(coords + i, d, n);
   const std::uint64_t h1 = key, h2 = bloom_mix(key ^ 0x5851f42d4c957f2dULL) | 1ULL;
   for (int k = 0; k < kBloomHashes; ++k) {
-    const std::uint64_t b = (h1 + static_cast<std::uint64_t>(k) * h2) % m;
+    const std::uint64_t b = bloom_bit(h1, h2, k, m);
     atomicOr(reinterpret_cast<unsigned long long*>(&bits[b >> 6]), 1ULL << (b & 63));
   }
 }
@@ -170,43 +170,88 @@ __global__ void __launch_bounds__(128) k_erase(const TreeSet ts, const double* _
   }
   std::uint64_t stk[kStack];
   const std::uint64_t key = bloom_key_reg<D>(p);
-  for (int t = 0; t < ts.count; ++t) {
-    if (ts.t[t].bloom && !bloom_test(ts.t[t].bloom, ts.t[t].bloom_bits, key)) continue;  // definitely absent
+  // candidate trees of this point: every bloom filter is tested up front (independent loads), then the
+  // lane walks its candidates one after another without waiting for the warp at tree boundaries.  (A
+  // loop over the trees with the warp reconverging per tree made every lane wait for each false
+  // positive's walk: at 1-2 % per lane and tree, about half of the warps walked every tree.)
+  unsigned long long cand = 0;
+  unsigned cand_hi = 0;  // trees 64.. (kMaxTrees = 66)
+  for (int t = 0; t < ts.count; ++t)
+    if (!ts.t[t].bloom || bloom_test(ts.t[t].bloom, ts.t[t].bloom_bits, key)) {  // else definitely absent
+      if (t < 64) cand |= 1ULL << t;
+      else cand_hi |= 1u << (t - 64);
+    }
+  while (cand | cand_hi) {
+    int t;
+    if (cand) {
+      t = __ffsll(static_cast<long long>(cand)) - 1;
+      cand &= cand - 1;
+    } else {
+      t = 64 + __ffs(static_cast<int>(cand_hi)) - 1;
+      cand_hi &= cand_hi - 1;
+    }
     const TNode<D>* nodes = static_cast<const TNode<D>*>(ts.t[t].tnodes);
     double* coords = const_cast<double*>(ts.t[t].coords);
     const std::uint64_t stride = ts.t[t].stride;
+    // the walk follows one child in a register; the stack (local memory) only takes the second child of a
+    // node whose two boxes both contain the point (boundary points, duplicates)
     int sp = 0;
-    stk[sp++] = ts.t[t].root;
+    std::uint64_t ref = ts.t[t].root;
     unsigned long long local = 0;
-    while (sp > 0) {
-      const std::uint64_t ref = stk[--sp];
+    while (true) {
       if (is_leaf_ref(ref)) {
         const std::uint32_t c = leaf_count(ref);
         const std::uint64_t s = leaf_start(ref);
-        for (std::uint32_t k = 0; k < c; ++k) {
-          // compare by value (so -0 == +0 as in the oracle), then swap exactly the bits that matched
-          const double c0 = coords[s + k];
-          bool eq = (c0 == p[0]);
+        // coordinate 0 of four points at a time (independent loads; the CAS below keeps the compiler from
+        // moving later loads above it, so one point per trip was one dependent round trip per point)
+        for (std::uint32_t k0 = 0; k0 < c; k0 += 4) {
+          double c0[4];
 #pragma unroll
-          for (int j = 1; j < D; ++j) eq = eq && (coords[j * stride + s + k] == p[j]);
-          if (eq) {
-            unsigned long long* a = reinterpret_cast<unsigned long long*>(&coords[s + k]);
-            const unsigned long long old = static_cast<unsigned long long>(__double_as_longlong(c0));
-            if (atomicCAS(a, old, 0x7ff8000000000000ULL) == old) ++local;
+          for (int u = 0; u < 4; ++u) c0[u] = k0 + u < c ? coords[s + k0 + u] : __longlong_as_double(0x7ff8000000000000LL);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // compare by value (so -0 == +0 as in the oracle), then swap exactly the bits that matched
+            bool eq = (c0[u] == p[0]);
+            if (!eq) continue;
+            const std::uint32_t k = k0 + u;
+#pragma unroll
+            for (int j = 1; j < D; ++j) eq = eq && (coords[j * stride + s + k] == p[j]);
+            if (eq) {
+              unsigned long long* a = reinterpret_cast<unsigned long long*>(&coords[s + k]);
+              const unsigned long long old = static_cast<unsigned long long>(__double_as_longlong(c0[u]));
+              if (atomicCAS(a, old, 0x7ff8000000000000ULL) == old) ++local;
+            }
           }
         }
+        if (sp == 0) break;
+        ref = stk[--sp];
         continue;
       }
-      const TNode<D>& nd = nodes[ref];
+      // the node in D + 1 16-byte loads: (lo0, lo1) and (hi0, hi1) per dimension pair, then the child refs
+      const float4* nd4 = reinterpret_cast<const float4*>(nodes + ref);
+      float4 w[D + 1];
 #pragma unroll
-      for (int s = 1; s >= 0; --s) {
-        bool in = true;
+      for (int v = 0; v <= D; ++v) w[v] = __ldg(nd4 + v);
+      const float* wf = reinterpret_cast<const float*>(w);  // lo[D][2], hi[D][2], ref[2]
+      const std::uint64_t* wr = reinterpret_cast<const std::uint64_t*>(w + D);
+      bool in[2];
 #pragma unroll
-        for (int j = 0; j < D; ++j) in = in && (pf_hi[j] >= nd.lo[j][s]) && (pf_lo[j] <= nd.hi[j][s]);
-        if (in) {
-          if (sp >= kStack) __trap();  // unreachable: tree depth <= kDepthCap + 31 < kStack
-          stk[sp++] = nd.ref[s];
-        }
+      for (int sd = 0; sd < 2; ++sd) {
+        in[sd] = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) in[sd] = in[sd] && (pf_hi[j] >= wf[2 * j + sd]) && (pf_lo[j] <= wf[2 * D + 2 * j + sd]);
+      }
+      if (in[0] && in[1]) {
+        if (sp >= kStack) __trap();  // unreachable: tree depth <= kDepthCap + 31 < kStack
+        stk[sp++] = wr[1];
+        ref = wr[0];
+      } else if (in[0]) {
+        ref = wr[0];
+      } else if (in[1]) {
+        ref = wr[1];
+      } else {
+        if (sp == 0) break;
+        ref = stk[--sp];
       }
     }
     if (local) atomicAdd(&killed[t], local);
@@ -564,7 +609,7 @@ struct gk_bdl {
       if (which[t] >= 0 && hk[t]) hit.push_back(&statics[which[t]]);
     for (std::size_t t = 0; t < which.size(); ++t)
       if (which[t] >= 0) statics[which[t]].live -= hk[t];
-    collapse_trees(d, hit, st);
+    collapse_trees(d, hit, st, bst, kBuildSlots);  // the trees' collapses run side by side on the build streams
     for (std::size_t t = 0; t < which.size(); ++t) {
       total += hk[t];
       if (which[t] >= 0) {

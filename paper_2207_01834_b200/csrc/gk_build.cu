@@ -1897,10 +1897,8 @@ __global__ void k_root_info(const std::int32_t* __restrict__ repl, const gk_cano
 }
 
 template <int D>
-void collapse_launch(DevTree& T, std::int32_t*& repl, std::uint32_t*& arrive, std::uint32_t* info, cudaStream_t st) {
+void collapse_launch(DevTree& T, std::int32_t* repl, std::uint32_t* arrive, std::uint32_t* info, cudaStream_t st) {
   const std::uint32_t N = static_cast<std::uint32_t>(T.n_nodes);
-  repl = dalloc<std::int32_t>(N, st);
-  arrive = dalloc<std::uint32_t>(N, st);
   GK_CUDA(cudaMemsetAsync(arrive, 0, static_cast<std::size_t>(N) * 4, st));
   k_collapse_up<<<blocks_for(N), 256, 0, st>>>(N, T.canon, T.coords, T.orig, repl, arrive);
   k_relink<D><<<blocks_for(N), 256, 0, st>>>(N, T.canon, static_cast<TNode<D>*>(T.tnodes), T.irank, T.orig, repl);
@@ -2253,7 +2251,7 @@ void collapse_tree(int d, DevTree& t, cudaStream_t st) {
 }
 
 // Erase_S collapses of several trees with one host round-trip for all their new roots
-void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st) {
+void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st, cudaStream_t* side, int nside) {
   std::vector<DevTree*> ts;
   for (DevTree* t : trees)
     if (t->n_nodes) ts.push_back(t);
@@ -2262,14 +2260,34 @@ void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st) 
   std::uint32_t* info = dalloc<std::uint32_t>(5 * m, st);
   std::vector<std::int32_t*> repl(m);
   std::vector<std::uint32_t*> arrive(m);
+  for (std::size_t i = 0; i < m; ++i) {  // stream-ordered on st; the side streams start after the fork event
+    repl[i] = dalloc<std::int32_t>(ts[i]->n_nodes, st);
+    arrive[i] = dalloc<std::uint32_t>(ts[i]->n_nodes, st);
+  }
+  const bool fork = side && nside > 0 && m > 1;
+  std::vector<cudaEvent_t> ev(fork ? m : 0);  // ev[0]: fork; ev[i]: tree i done on its side stream
+  if (fork) {
+    for (auto& e : ev) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    GK_CUDA(cudaEventRecord(ev[0], st));
+  }
   for (std::size_t i = 0; i < m; ++i) {
+    cudaStream_t s = st;
+    if (fork && i > 0) {
+      s = side[(i - 1) % static_cast<std::size_t>(nside)];
+      GK_CUDA(cudaStreamWaitEvent(s, ev[0], 0));
+    }
     switch (d) {
-#define GK_D(DD) case DD: collapse_launch<DD>(*ts[i], repl[i], arrive[i], info + 5 * i, st); break;
+#define GK_D(DD) case DD: collapse_launch<DD>(*ts[i], repl[i], arrive[i], info + 5 * i, s); break;
       GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
 #undef GK_D
       default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
     }
+    if (fork && i > 0) {
+      GK_CUDA(cudaEventRecord(ev[i], s));
+      GK_CUDA(cudaStreamWaitEvent(st, ev[i], 0));
+    }
   }
+  for (auto& e : ev) GK_CUDA(cudaEventDestroy(e));
   std::vector<std::uint32_t> h(5 * m);
   GK_CUDA(cudaMemcpyAsync(h.data(), info, 5 * m * 4, cudaMemcpyDeviceToHost, st));
   GK_CUDA(cudaStreamSynchronize(st));

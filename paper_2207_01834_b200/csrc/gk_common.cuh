@@ -131,13 +131,25 @@ __device__ inline std::uint64_t bloom_key_reg(const double (&x)[D]) {
   }
   return z;
 }
-__device__ inline bool bloom_test(const std::uint64_t* bits, std::uint64_t m, std::uint64_t key) {
+// probe i of a key: bit floor(h_i m / 2^64) of the m-bit filter, h_i = h1 + i h2 (multiply-shift range
+// reduction: one 64 x 64 -> high-64 multiply; a 64-bit `% m` costs ~100 instructions per probe on the GPU)
+__device__ __forceinline__ std::uint64_t bloom_bit(std::uint64_t h1, std::uint64_t h2, int i, std::uint64_t m) {
+  return __umul64hi(h1 + static_cast<std::uint64_t>(i) * h2, m);
+}
+// two probes first (their loads in flight together; an absent key leaves after them three times out of
+// four), then the other five together
+__device__ inline bool bloom_test(const std::uint64_t* __restrict__ bits, std::uint64_t m, std::uint64_t key) {
   const std::uint64_t h1 = key, h2 = bloom_mix(key ^ 0x5851f42d4c957f2dULL) | 1ULL;
-  for (int i = 0; i < kBloomHashes; ++i) {
-    const std::uint64_t b = (h1 + static_cast<std::uint64_t>(i) * h2) % m;
-    if (!((bits[b >> 6] >> (b & 63)) & 1ULL)) return false;
+  const std::uint64_t b0 = bloom_bit(h1, h2, 0, m), b1 = bloom_bit(h1, h2, 1, m);
+  const std::uint64_t w0 = bits[b0 >> 6], w1 = bits[b1 >> 6];
+  if (!((w0 >> (b0 & 63)) & (w1 >> (b1 & 63)) & 1ULL)) return false;
+  std::uint64_t all = 1ULL;
+#pragma unroll
+  for (int i = 2; i < kBloomHashes; ++i) {
+    const std::uint64_t b = bloom_bit(h1, h2, i, m);
+    all &= bits[b >> 6] >> (b & 63);
   }
-  return true;
+  return (all & 1ULL) != 0;
 }
 constexpr int kMaxTrees = 66;
 struct TreeSet {
@@ -186,7 +198,10 @@ void free_tree(DevTree& t, cudaStream_t st);
 // nodes and the traversal nodes and updates root_slot / root_ref.
 void collapse_tree(int d, DevTree& t, cudaStream_t st);
 // the same for several trees, one host round-trip for all their new roots
-void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st);
+// side streams (optional): the trees' collapses are independent, so all but the first run on them, forked
+// from and joined to st by events
+void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st, cudaStream_t* side = nullptr,
+                    int nside = 0);
 
 // knn.cu
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq,
