@@ -609,7 +609,9 @@ struct gk_bdl {
       if (which[t] >= 0 && hk[t]) hit.push_back(&statics[which[t]]);
     for (std::size_t t = 0; t < which.size(); ++t)
       if (which[t] >= 0) statics[which[t]].live -= hk[t];
-    collapse_trees(d, hit, st, bst, kBuildSlots);  // the trees' collapses run side by side on the build streams
+    // the static trees' collapses run side by side on the build streams while st compacts and rebuilds the buffer
+    CollapseJob cjob;
+    collapse_trees_begin(cjob, d, hit, st, bst, kBuildSlots);
     for (std::size_t t = 0; t < which.size(); ++t) {
       total += hk[t];
       if (which[t] >= 0) {
@@ -639,6 +641,7 @@ struct gk_bdl {
         rebuild_buffer_tree();
       }
     }
+    collapse_trees_finish(cjob);
     // trees below half of their build size are gathered into R and reinserted
     std::uint64_t rn = 0;
     for (int i = 0; i < 64; ++i)

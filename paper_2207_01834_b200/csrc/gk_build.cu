@@ -2251,55 +2251,69 @@ void collapse_tree(int d, DevTree& t, cudaStream_t st) {
 }
 
 // Erase_S collapses of several trees with one host round-trip for all their new roots
-void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st, cudaStream_t* side, int nside) {
-  std::vector<DevTree*> ts;
+void collapse_trees_begin(CollapseJob& job, int d, const std::vector<DevTree*>& trees, cudaStream_t st,
+                          cudaStream_t* side, int nside) {
+  job = CollapseJob();
+  job.st = st;
   for (DevTree* t : trees)
-    if (t->n_nodes) ts.push_back(t);
-  if (ts.empty()) return;
-  const std::size_t m = ts.size();
-  std::uint32_t* info = dalloc<std::uint32_t>(5 * m, st);
-  std::vector<std::int32_t*> repl(m);
-  std::vector<std::uint32_t*> arrive(m);
+    if (t->n_nodes) job.ts.push_back(t);
+  if (job.ts.empty()) return;
+  const std::size_t m = job.ts.size();
+  job.info = dalloc<std::uint32_t>(5 * m, st);
+  job.repl.resize(m);
+  job.arrive.resize(m);
   for (std::size_t i = 0; i < m; ++i) {  // stream-ordered on st; the side streams start after the fork event
-    repl[i] = dalloc<std::int32_t>(ts[i]->n_nodes, st);
-    arrive[i] = dalloc<std::uint32_t>(ts[i]->n_nodes, st);
+    job.repl[i] = dalloc<std::int32_t>(job.ts[i]->n_nodes, st);
+    job.arrive[i] = dalloc<std::uint32_t>(job.ts[i]->n_nodes, st);
   }
-  const bool fork = side && nside > 0 && m > 1;
-  std::vector<cudaEvent_t> ev(fork ? m : 0);  // ev[0]: fork; ev[i]: tree i done on its side stream
+  const bool fork = side && nside > 0;
   if (fork) {
-    for (auto& e : ev) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    GK_CUDA(cudaEventRecord(ev[0], st));
+    job.ev.resize(m + 1);
+    for (auto& e : job.ev) GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    GK_CUDA(cudaEventRecord(job.ev[0], st));
   }
   for (std::size_t i = 0; i < m; ++i) {
     cudaStream_t s = st;
-    if (fork && i > 0) {
-      s = side[(i - 1) % static_cast<std::size_t>(nside)];
-      GK_CUDA(cudaStreamWaitEvent(s, ev[0], 0));
+    if (fork) {
+      s = side[i % static_cast<std::size_t>(nside)];
+      GK_CUDA(cudaStreamWaitEvent(s, job.ev[0], 0));
     }
     switch (d) {
-#define GK_D(DD) case DD: collapse_launch<DD>(*ts[i], repl[i], arrive[i], info + 5 * i, s); break;
+#define GK_D(DD) case DD: collapse_launch<DD>(*job.ts[i], job.repl[i], job.arrive[i], job.info + 5 * i, s); break;
       GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
 #undef GK_D
       default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
     }
-    if (fork && i > 0) {
-      GK_CUDA(cudaEventRecord(ev[i], s));
-      GK_CUDA(cudaStreamWaitEvent(st, ev[i], 0));
-    }
+    if (fork) GK_CUDA(cudaEventRecord(job.ev[1 + i], s));
   }
-  for (auto& e : ev) GK_CUDA(cudaEventDestroy(e));
+}
+
+void collapse_trees_finish(CollapseJob& job) {
+  if (job.ts.empty()) return;
+  cudaStream_t st = job.st;
+  const std::size_t m = job.ts.size();
+  for (std::size_t i = 1; i < job.ev.size(); ++i) GK_CUDA(cudaStreamWaitEvent(st, job.ev[i], 0));
+  for (auto& e : job.ev) GK_CUDA(cudaEventDestroy(e));
+  job.ev.clear();
   std::vector<std::uint32_t> h(5 * m);
-  GK_CUDA(cudaMemcpyAsync(h.data(), info, 5 * m * 4, cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaMemcpyAsync(h.data(), job.info, 5 * m * 4, cudaMemcpyDeviceToHost, st));
   GK_CUDA(cudaStreamSynchronize(st));
   for (std::size_t i = 0; i < m; ++i) {
-    DevTree& T = *ts[i];
+    DevTree& T = *job.ts[i];
     const std::int32_t root = static_cast<std::int32_t>(h[5 * i]);
     T.root_slot = root;
     if (root >= 0) T.root_ref = h[5 * i + 1] == 1 ? make_leaf_ref(h[5 * i + 2], h[5 * i + 3]) : h[5 * i + 4];
-    dfree(repl[i], st);
-    dfree(arrive[i], st);
+    dfree(job.repl[i], st);
+    dfree(job.arrive[i], st);
   }
-  dfree(info, st);
+  dfree(job.info, st);
+  job.ts.clear();
+}
+
+void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st, cudaStream_t* side, int nside) {
+  CollapseJob job;
+  collapse_trees_begin(job, d, trees, st, side, nside);
+  collapse_trees_finish(job);
 }
 
 void free_tree(DevTree& t, cudaStream_t st) {

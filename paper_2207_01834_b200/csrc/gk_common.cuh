@@ -198,8 +198,21 @@ void free_tree(DevTree& t, cudaStream_t st);
 // nodes and the traversal nodes and updates root_slot / root_ref.
 void collapse_tree(int d, DevTree& t, cudaStream_t st);
 // the same for several trees, one host round-trip for all their new roots
-// side streams (optional): the trees' collapses are independent, so all but the first run on them, forked
-// from and joined to st by events
+// The trees' collapses are independent.  With side streams every tree's kernels run on one of them, forked
+// from st by an event, so that st stays free for the caller's own work (Erase_L compacts and rebuilds the
+// buffer meanwhile); collapse_trees_finish joins them into st, reads the new roots back (one host
+// round-trip) and releases the temporaries.
+struct CollapseJob {
+  std::vector<DevTree*> ts;
+  std::uint32_t* info = nullptr;
+  std::vector<std::int32_t*> repl;
+  std::vector<std::uint32_t*> arrive;
+  std::vector<cudaEvent_t> ev;  // [0]: fork; [1 + i]: tree i done
+  cudaStream_t st = nullptr;
+};
+void collapse_trees_begin(CollapseJob& job, int d, const std::vector<DevTree*>& trees, cudaStream_t st,
+                          cudaStream_t* side = nullptr, int nside = 0);
+void collapse_trees_finish(CollapseJob& job);
 void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st, cudaStream_t* side = nullptr,
                     int nside = 0);
 
