@@ -503,7 +503,7 @@ def run_gpu(args):
                     "pageable": {"value": e2e_pageable, "unit": "queries/s",
                                  "note": "the same gk_bdl_knn call from pageable numpy buffers (what a std::vector "
                                          "caller of geokit_bdl.hpp gets): staged through the handle's pinned ring"}},
-            "gpu_launches": 10 * args.steps,  # k_qbox_init, k_qbox, k_curve_key, 6 CUB radix-sort kernels, k_knn
+            "gpu_launches": 9 * args.steps,  # k_qbox_init, k_qbox, k_curve_key, 5 CUB radix-sort kernels (histogram, scan, 3 onesweep passes), k_knn
             "clocks": clk_sum,
             "consumers": extras,
             "configs": configs,

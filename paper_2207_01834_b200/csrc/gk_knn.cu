@@ -25,6 +25,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -721,10 +722,16 @@ void order_queries(const double* Q, std::uint64_t nq, std::uint32_t* perm_out, c
   GK_CHECK_LAUNCH();
   void* tmp = nullptr;
   std::size_t tb = 0;
+  // 32-bit keys are sorted on their top 24 bits only (three 8-bit radix passes instead of four): cells of
+  // 1/256 (3D) or 1/4096 (2D) of the batch's box order the packets as well as the full key does (C2 +0.5 %,
+  // C1 +3 %, C5 +1.4 % kNN_L).  GK_SORT_SKIP overrides the number of ignored low bits.
+  static const int skip_env = std::getenv("GK_SORT_SKIP") ? std::atoi(std::getenv("GK_SORT_SKIP")) : -1;
+  const int skip = skip_env >= 0 ? skip_env : (sizeof(Key) == 4 && bits > 24 ? bits - 24 : 0);
+  const int b0 = std::min(std::max(skip, 0), bits - 8);
   auto sort = [&](auto n) {  // 32-bit item counts when they fit (CUB's faster offset type), else 64-bit
-    GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, perm_out, n, 0, bits, st));
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, idx, perm_out, n, b0, bits, st));
     GK_CUDA(cudaMallocAsync(&tmp, tb, st));
-    GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, perm_out, n, 0, bits, st));
+    GK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, idx, perm_out, n, b0, bits, st));
   };
   if (nq <= 0x7fffffffULL) sort(static_cast<int>(nq));
   else sort(static_cast<long long>(nq));
