@@ -1640,7 +1640,25 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
       nb.hi[static_cast<std::uint64_t>(y) * D + j] = __ldcg(&na.hi[static_cast<std::uint64_t>(x) * D + j]);
     }
   }
-  // scatter the subtrees' nodes: one warp per subtree, level by level
+  // scatter the subtrees' nodes: one warp per subtree, level by level.  Their parent / first-child links
+  // follow from the subtree's own level-major layout (an internal node's children are records 2 p, 2 p + 1
+  // of the subtree's next level, p = internal nodes before it in its level; a leaf's insertion point among
+  // the next level is the same 2 p), so only the level loop's nodes need the binary searches below
+  // (1.4M nodes x two ~17-step searches were ~40 % of k_merge on C2's largest tree)
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // merged index of the first node of subtree (rs = first point, k = root rank) at level l (or, where it
+  // has none, of the position its nodes would take): level offset + subtree nodes of roots left of it +
+  // level-loop nodes left of it
+  auto sub_level_base = [&](int l, std::uint32_t rs, std::uint32_t k) -> std::uint32_t {
+    if (l >= H) return __ldcg(&a.new_off[H]);
+    std::uint32_t y = __ldcg(&a.new_off[l]);
+    if (l > Lmin) {
+      const std::uint32_t row = (l - Lmin - 1) * R;
+      y += __ldcg(&a.V[row + k]) - __ldcg(&a.V[row]);
+    }
+    if (l < HA) y += lower_bound_u32(na.start, __ldcg(&a.lvl_off[l]), __ldcg(&a.lvl_off[l + 1]), rs) - __ldcg(&a.lvl_off[l]);
+    return y;
+  };
   for (std::uint32_t r = gwarp; r < R; r += nwarps) {
     const std::uint32_t g = __ldcg(&a.small_list[r]);
     const std::uint32_t rs = __ldcg(&na.start[g]);
@@ -1648,18 +1666,38 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
     const int nlev = static_cast<int>(__ldcg(&a.sub_nlev[r]));
     const std::uint32_t k = root_rank(rs);
     std::uint32_t src = __ldcg(&a.sub_base[r]);
+    // the root is the level loop's node g: its merged index (as in the scatter above)
+    std::uint32_t yg = __ldcg(&a.new_off[L]) + (g - __ldcg(&a.lvl_off[L]));
+    if (L > Lmin) {
+      const std::uint32_t row = (L - Lmin - 1) * R;
+      yg += __ldcg(&a.V[row + k]) - __ldcg(&a.V[row]);
+    }
+    std::uint32_t y0 = nlev > 1 ? sub_level_base(L + 1, rs, k) : 0u;
     for (int lam = 1; lam < nlev; ++lam) {
       const int l = L + lam;
       const std::uint32_t cnt = __ldcg(&a.sub_cnt[static_cast<std::uint64_t>(r) * kSubLevels + lam]);
-      const std::uint32_t row = (l - Lmin - 1) * R;
-      std::uint32_t y0 = __ldcg(&a.new_off[l]) + __ldcg(&a.V[row + k]) - __ldcg(&a.V[row]);
-      if (l < HA) y0 += lower_bound_u32(na.start, __ldcg(&a.lvl_off[l]), __ldcg(&a.lvl_off[l + 1]), rs) - __ldcg(&a.lvl_off[l]);
-      for (std::uint32_t j = lane; j < cnt; j += 32) {
+      const std::uint32_t y0n = sub_level_base(l + 1, rs, k);
+      if (lam == 1 && lane < static_cast<int>(cnt)) nb.parent[y0 + lane] = yg;  // the root's two children
+      std::uint32_t carry = 0;  // internal nodes of this level before the current round
+      for (std::uint32_t jb = 0; jb < cnt; jb += 32) {
+        const std::uint32_t j = jb + lane;
+        const bool valid = j < cnt;
         const std::uint32_t xs = src + j, y = y0 + j;
-        GK_ASSERT(y < 2 * n - 1 && xs < 2 * n);
+        GK_ASSERT(!valid || (y < 2 * n - 1 && xs < 2 * n));
+        const std::uint8_t fl = valid ? __ldcg(&a.s_flags[xs]) : F_LEAF;
+        const bool internal = valid && !(fl & F_LEAF);
+        const unsigned bal = __ballot_sync(0xffffffffu, internal);
+        const std::uint32_t cb = y0n + 2 * (carry + __popc(bal & lt_mask));
+        carry += __popc(bal);
+        if (!valid) continue;
+        nb.cbase[y] = cb;
+        if (internal) {
+          nb.parent[cb] = y;
+          nb.parent[cb + 1] = y;
+        }
         nb.start[y] = __ldcg(&a.s_start[xs]);
         nb.count[y] = __ldcg(&a.s_count[xs]);
-        nb.flags[y] = __ldcg(&a.s_flags[xs]);
+        nb.flags[y] = fl;
         nb.level[y] = static_cast<std::uint8_t>(l);
         nb.split[y] = __ldcg(&a.s_split[xs]);
 #pragma unroll
@@ -1669,15 +1707,21 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
         }
       }
       src += cnt;
+      y0 = y0n;
     }
   }
   sync_all(grid);
   GK_MSTAMP();
-  // parent / first child (or, for a leaf, the insertion point among the next level) by start
-  const std::uint32_t Nall = __ldcg(&a.new_off[H]);
-  for (std::uint32_t x = gtid; x < Nall; x += gthreads) {
-    const int l = __ldcg(&nb.level[x]);
-    const std::uint32_t st = __ldcg(&nb.start[x]);
+  // parent / first child (or, for a leaf, the insertion point among the next level) of the level loop's
+  // nodes, by start
+  for (std::uint32_t x0 = gtid; x0 < NA; x0 += gthreads) {
+    const int l = __ldcg(&na.level[x0]);
+    const std::uint32_t st = __ldcg(&na.start[x0]);
+    std::uint32_t x = __ldcg(&a.new_off[l]) + (x0 - __ldcg(&a.lvl_off[l]));  // its merged index (as scattered)
+    if (l > Lmin) {
+      const std::uint32_t row = (l - Lmin - 1) * R;
+      x += __ldcg(&a.V[row + root_rank(st)]) - __ldcg(&a.V[row]);
+    }
     GK_ASSERT(l < H && st < n);
     const std::uint32_t o1 = __ldcg(&a.new_off[l + 1]), o2 = __ldcg(&a.new_off[l + 2 <= H ? l + 2 : H]);
     nb.cbase[x] = (l + 1 < H) ? lower_bound_u32(nb.start, o1, o2, st) : o1;
