@@ -142,6 +142,7 @@ struct BuildArgs {
   std::uint32_t* hist;      // [kSelCap * 256]
   std::uint32_t* bsum;      // [3 * gridDim + 2]
   std::uint32_t* int_by_slot;  // [cap + 1]
+  std::uint32_t* irank_slot;   // [cap + 1] slot -> internal rank (k_emit copies it into the tree)
   // bottom phase (k_subtree + k_merge): subtrees of nodes with leaf < count <= Tsmall, one block each
   std::uint32_t Tsmall;        // 0: off (object-median heuristic, leaf < 4, or a tree that fits no block)
   std::uint32_t rmax;          // capacity of the small-root arrays
@@ -246,8 +247,9 @@ __device__ void grid_scan(cg::grid_group& grid, const std::uint32_t* in, std::ui
 // exactly one frame (d0, l) of the recursion; its root r is d's ancestor at depth d0, and
 // pos(v) = pos(r) + |top part of the frame| + sizes of the bottom subtrees left of v's, all
 // restricted to the frame's levels (range propagation).  Writes ctrl[C_H] / ctrl[C_N] and the
-// slot -> internal flags k_slot_rank scans into TNode indices.
-__device__ void veb_phase(cg::grid_group& grid, const BuildArgs& a, const NodeArrays& na, std::uint32_t* lvl_off, int H) {
+// slot -> internal flags, scanned into TNode indices (a.irank_slot) at the end.
+__device__ void veb_phase(cg::grid_group& grid, const BuildArgs& a, const NodeArrays& na, std::uint32_t* lvl_off, int H,
+                          std::uint32_t* sh) {
   const std::uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const std::uint32_t gthreads = gridDim.x * blockDim.x;
   const std::uint32_t N = __ldcg(&lvl_off[H]);
@@ -293,11 +295,15 @@ __device__ void veb_phase(cg::grid_group& grid, const BuildArgs& a, const NodeAr
     }
     sync_all(grid);
   }
-  // slot -> internal flag (scanned into internal ranks = TNode indices by k_slot_rank)
+  // slot -> internal flag
   for (std::uint32_t g = gtid; g <= N; g += gthreads) {
     if (g == N) a.int_by_slot[N] = 0;
     else a.int_by_slot[__ldcg(&na.pos[g])] = (__ldcg(&na.flags[g]) & F_LEAF) ? 0u : 1u;
   }
+  // ... scanned into internal ranks (= TNode indices) here, in the same launch (a cooperative k_slot_rank
+  // launch after the host learned N used to do it: ~25 us on every tree's critical path)
+  sync_all(grid);
+  grid_scan(grid, a.int_by_slot, a.irank_slot, N + 1, a.bsum, sh);
 }
 
 // -------------------------------------------------------------- the build --
@@ -1065,7 +1071,7 @@ __global__ void __launch_bounds__(kThreads, (D <= 4 ? GK_BUILD_MINB : GK_BUILD_M
     GK_TL_PRINT(level0);
     return;
   }
-  veb_phase(grid, a, na, a.lvl_off, level);
+  veb_phase(grid, a, na, a.lvl_off, level, sh);
 #if GK_BUILD_TIMELINE
   if (gtid == 0) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tv_b));
@@ -1734,7 +1740,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
   }
   sync_all(grid);
   GK_MSTAMP();
-  veb_phase(grid, a, nb, a.new_off, H);
+  veb_phase(grid, a, nb, a.new_off, H, sh);
   GK_MSTAMP();
 #if GK_BUILD_TIMELINE
   if (gtid == 0) {
@@ -1746,12 +1752,6 @@ __global__ void __launch_bounds__(kThreads) k_merge(const BuildArgs a) {
 #undef GK_MSTAMP
 }
 
-__global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::uint32_t* irank_by_slot) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ std::uint32_t sh[32];
-  const std::uint32_t N = __ldcg(&a.ctrl[C_N]);
-  grid_scan(grid, a.int_by_slot, irank_by_slot, N + 1, a.bsum, sh);
-}
 
 // One thread per node (level-array order, so the node-array reads coalesce); the canonical record and
 // the traversal node are staged in shared memory and written by the whole warp, 8 / 16 bytes per lane
@@ -1759,15 +1759,16 @@ __global__ void __launch_bounds__(kThreads) k_slot_rank(const BuildArgs a, std::
 // touching 32 sectors: k_emit took 337 us on C2's largest tree)
 constexpr int kEmitThreads = 128;
 template <int D>
-__global__ void __launch_bounds__(kEmitThreads) k_emit(const BuildArgs a, std::uint32_t N,
-                                                      const std::uint32_t* __restrict__ irank_by_slot,
+__global__ void __launch_bounds__(kEmitThreads) k_emit(const BuildArgs a, std::uint32_t N, std::uint32_t* __restrict__ irank_out,
                                                       gk_canon_node* canon, TNode<D>* tn, std::int32_t* orig) {
+  const std::uint32_t* __restrict__ irank_by_slot = a.irank_slot;  // scanned at the end of the vEB phase
   static_assert(sizeof(gk_canon_node) % 8 == 0 && sizeof(TNode<D>) % 16 == 0, "record sizes");
   __shared__ gk_canon_node s_c[kEmitThreads];
   __shared__ TNode<D> s_t[kEmitThreads];
   __shared__ std::uint32_t s_slot[kEmitThreads], s_ti[kEmitThreads];
   const NodeArrays& na = a.na;
   const std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g <= N) irank_out[g] = irank_by_slot[g];  // the tree's own copy (erase collapse relinks through it)
   if (g < N) {
     const std::uint32_t slot = na.pos[g];
     const std::uint8_t fl = na.flags[g];
@@ -1986,7 +1987,7 @@ std::size_t scratch_bytes(std::uint64_t n, std::uint64_t cap_chunks, int G) {
   const std::uint64_t cap = 2 * n - 1, cap_level = std::min<std::uint64_t>(cap, n);
   return 2 * n * D * 8 + 2 * n * 4 + cap * (7 * 4 + 2 + 8 + 2 * D * 8) + 4 * (cap + 1) + (cap_level + 1) * 4 * 7 +
          cap_chunks * 4 * 4 + cap_level * D * 2 * 8 + (kMaxLevels + 2) * 4 + C_COUNT * 4 + kSelCap * sizeof(SelState) +
-         kSelCap * 256 * 4 + (3 * G + 2) * 4 + 4 * (cap + 1) + 44 * 256;
+         kSelCap * 256 * 4 + (3 * G + 2) * 4 + 8 * (cap + 1) + 46 * 256;
 }
 
 // the bottom phase's arrays (small roots, subtree node records, merge scratch, merged level arrays)
@@ -2099,6 +2100,7 @@ void build_begin_d(BuildScratch& sc, int leaf, int heuristic, const double* src,
   a.hist = reinterpret_cast<std::uint32_t*>(take(kSelCap * 256 * 4));
   a.bsum = reinterpret_cast<std::uint32_t*>(take((3 * G + 2) * 4));
   a.int_by_slot = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
+  a.irank_slot = reinterpret_cast<std::uint32_t*>(take((cap + 1) * 4));
   a.Tsmall = bottom ? static_cast<std::uint32_t>(small_cap<D>()) : 0u;
   if (bottom) {
     const std::uint64_t rmax = n / (leaf + 1) + 1;
@@ -2172,7 +2174,6 @@ void build_finish_d(BuildScratch& sc) {
   DevTree& T = *sc.out;
   cudaStream_t st = sc.st;
   const std::uint64_t n = sc.n;
-  const int G = sc.grid;
   GK_CUDA(cudaStreamSynchronize(st));
   const int H = static_cast<int>(sc.host_ctrl[C_H]);
   const std::uint32_t N = sc.host_ctrl[C_N];
@@ -2185,13 +2186,9 @@ void build_finish_d(BuildScratch& sc) {
   T.tnodes = dalloc<TNode<D>>(T.n_internal, st);
   T.orig = dalloc<std::int32_t>(3 * static_cast<std::uint64_t>(N), st);
   GK_CUDA(cudaMemsetAsync(T.orig + 2 * static_cast<std::uint64_t>(N), 0xff, 4, st));  // parent(root) = -1
-  std::uint32_t* irank_ptr = T.irank;
-  void* args2[] = {&a, &irank_ptr};
-  const int G2 = static_cast<int>(std::min<std::uint64_t>(G, std::max<std::uint64_t>(1, N / 4096)));
-  GK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_slot_rank), dim3(G2), dim3(kThreads), args2, 0, st));
   BuildArgs ea = a;  // after the bottom phase the merged level arrays are a.na2
   if (sc.host_ctrl[C_NSMALL] > 0) ea.na = a.na2;
-  k_emit<D><<<(N + kEmitThreads - 1) / kEmitThreads, kEmitThreads, 0, st>>>(ea, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
+  k_emit<D><<<(N + 1 + kEmitThreads - 1) / kEmitThreads, kEmitThreads, 0, st>>>(ea, N, T.irank, T.canon, static_cast<TNode<D>*>(T.tnodes), T.orig);
   GK_CHECK_LAUNCH();
   T.root_ref = (N == 1) ? make_leaf_ref(0, static_cast<std::uint32_t>(n)) : 0;
   T.root_slot = 0;
