@@ -1050,28 +1050,38 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
       // H2D of every chunk on pst[0], kNN_L of chunk i on st once its queries landed, D2H of chunk i on
       // pst[1] once its rows are final.  Each chunk is Hilbert-ordered on its own; results are
       // bit-identical to the one-shot path.
-      while (h->pev.size() < 2 * nck + 2) {
+      // The K2 order of chunk c + 1 runs on a side stream (the first build stream) as soon as its queries
+      // landed: its kernels fill the SMs that chunk c's persistent K1 blocks leave at its tail, instead of
+      // starting after it (5 x ~0.25 ms on the compute stream's chain).
+      while (h->pev.size() < 3 * nck + 2) {
         cudaEvent_t e;
         GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         h->pev.push_back(e);
       }
       cudaEvent_t ev_alloc = h->pev[0], ev_done = h->pev[1];
+      cudaEvent_t* ev_ord = h->pev.data() + 2 + 2 * nck;
+      cudaStream_t ost = h->bst[0];
       double* dq = dalloc<double>(nq * h->d, h->st);
       std::uint32_t* di = dalloc<std::uint32_t>(nq * k, h->st);
       double* dd = dalloc<double>(nq * k, h->st);
+      std::uint32_t* dperm = dalloc<std::uint32_t>(nq, h->st);
       GK_CUDA(cudaEventRecord(ev_alloc, h->st));
       GK_CUDA(cudaStreamWaitEvent(h->pst[0], ev_alloc, 0));
       GK_CUDA(cudaStreamWaitEvent(h->pst[1], ev_alloc, 0));
+      GK_CUDA(cudaStreamWaitEvent(ost, ev_alloc, 0));
       for (std::uint64_t c = 0; c < nck; ++c) {
         const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
         GK_CUDA(cudaMemcpyAsync(dq + off * h->d, q + off * h->d, m * h->d * sizeof(double), cudaMemcpyHostToDevice,
                                 h->pst[0]));
         GK_CUDA(cudaEventRecord(h->pev[2 + 2 * c], h->pst[0]));
+        GK_CUDA(cudaStreamWaitEvent(ost, h->pev[2 + 2 * c], 0));
+        range_order(h->d, dq + off * h->d, m, dperm + off, ost);
+        GK_CUDA(cudaEventRecord(ev_ord[c], ost));
       }
       for (std::uint64_t c = 0; c < nck; ++c) {
         const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
-        GK_CUDA(cudaStreamWaitEvent(h->st, h->pev[2 + 2 * c], 0));
-        knn_launch(h->d, k, ts, dq + off * h->d, m, di + off * k, dd + off * k, nullptr, h->st, nullptr, nullptr);
+        GK_CUDA(cudaStreamWaitEvent(h->st, ev_ord[c], 0));
+        knn_traverse(h->d, k, ts, dq + off * h->d, dperm + off, m, di + off * k, dd + off * k, h->st);
         GK_CUDA(cudaEventRecord(h->pev[3 + 2 * c], h->st));
         GK_CUDA(cudaStreamWaitEvent(h->pst[1], h->pev[3 + 2 * c], 0));
         GK_CUDA(cudaMemcpyAsync(ids + off * k, di + off * k, m * k * sizeof(std::uint32_t), cudaMemcpyDeviceToHost,
@@ -1083,6 +1093,7 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
       dfree(dq, h->st);
       dfree(di, h->st);
       dfree(dd, h->st);
+      dfree(dperm, h->st);
       GK_CUDA(cudaStreamSynchronize(h->st));
       return;
     }

@@ -220,6 +220,8 @@ void collapse_trees(int d, const std::vector<DevTree*>& trees, cudaStream_t st, 
 void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::uint64_t nq,
                 std::uint32_t* ids_dev, double* d2_dev, gk_knn_counters* counters, cudaStream_t st,
                 cudaEvent_t ev_k0, cudaEvent_t ev_k1, const double* bound = nullptr);
+void knn_traverse(int d, int k, const TreeSet& trees, const double* q_dev, const std::uint32_t* perm, std::uint64_t nq,
+                  std::uint32_t* ids_dev, double* d2_dev, cudaStream_t st);
 // range search (ball, d2 <= r2): K2 order, count / fill passes over the same order, per-query sort
 void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st);
 // mode 0: counts; 1: rows at offs; 2: the first capq rows of query i at ids/d2 + i * capq, and counts

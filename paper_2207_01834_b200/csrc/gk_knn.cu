@@ -1136,6 +1136,21 @@ void knn_launch(int d, int k, const TreeSet& trees, const double* q_dev, std::ui
   GK_CUDA(cudaFreeAsync(perm, st));
 }
 
+// K1 alone over queries already ordered by range_order (the pinned host pipeline orders chunk c + 1 on a
+// side stream while chunk c is traversed)
+void knn_traverse(int d, int k, const TreeSet& trees, const double* q_dev, const std::uint32_t* perm, std::uint64_t nq,
+                  std::uint32_t* ids_dev, double* d2_dev, cudaStream_t st) {
+  if (nq == 0) return;
+  if (nq >= 0xffffffffULL) throw Error(GK_ERR_INVALID, "kNN batch larger than 2^32-1 queries");
+  switch (d) {
+#define GK_D(DD) case DD: launch_d<DD>(k, trees, q_dev, perm, nq, ids_dev, d2_dev, nullptr, st, nullptr); break;
+    GK_D(2) GK_D(3) GK_D(4) GK_D(5) GK_D(6) GK_D(7) GK_D(8)
+#undef GK_D
+    default: throw Error(GK_ERR_INVALID, "unsupported dimension " + std::to_string(d));
+  }
+  GK_CHECK_LAUNCH();
+}
+
 void range_order(int d, const double* q_dev, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st) {
   switch (d) {
 #define GK_D(DD) case DD: order_queries<DD>(q_dev, nq, perm, st); break;
