@@ -698,6 +698,7 @@ void launch_d(int k, const TreeSet& ts, const double* Q, const std::uint32_t* pe
   else if (k <= 5) launch_k<D, 5>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
   else if (k <= 8) launch_k<D, 8>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
   else if (k <= 10) launch_k<D, 10>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
+  else if (k <= 12) launch_k<D, 12>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);  // k + 1 = 11: the k = 10 k-NN graph
   else if (k <= 16) launch_k<D, 16>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
   else if (k <= 32) launch_k<D, 32>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
   else if (k <= kMaxRuntimeK) launch_k<D, 0>(ts, Q, perm, nq, k, ids, d2, ctr, st, bound);
