@@ -1172,11 +1172,17 @@ __device__ __forceinline__ void warp_minmax(unsigned long long& mn, unsigned lon
 // partition (the children's min/max in the next level's dimension accumulate while it partitions);
 // leaves reduce their full box; internal nodes' full boxes are the unions of their children's,
 // bottom-up after the last level.
-constexpr int kSubBig = 128;
+// nodes of up to this many points are split by one warp (1, 2, 4 or 8 rounds of 32 points), larger ones by the
+// whole block one after another: 256 instead of 128 moves a 1024-point subtree's four 256-point nodes from the
+// block path (~8 block barriers per node) to four warps side by side (C2 Insert_L 5.13 -> 5.00 ms, C1 -3.5 %)
+#ifndef GK_SUB_BIG
+#define GK_SUB_BIG 256
+#endif
+constexpr int kSubBig = GK_SUB_BIG;
 template <int D>
 __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
   constexpr int T = small_cap<D>(), NM = small_nmax<D>();
-  static_assert(kSubBig <= 128, "warp-mode nodes take at most 4 rounds of 32 points");
+  static_assert(kSubBig <= 256, "warp-mode nodes take at most 8 rounds of 32 points");
   extern __shared__ __align__(16) unsigned char smem[];
   double* X = reinterpret_cast<double*>(smem);                                        // [D][T]
   unsigned long long* nbl = reinterpret_cast<unsigned long long*>(X + D * T);          // [2][NM] split-dim lo key
@@ -1388,7 +1394,8 @@ __global__ void __launch_bounds__(kSubThreads) k_subtree(const BuildArgs a) {
         };
         if (cnt <= 32) split_node(std::integral_constant<int, 1>{});
         else if (cnt <= 64) split_node(std::integral_constant<int, 2>{});
-        else split_node(std::integral_constant<int, 4>{});
+        else if (kSubBig <= 128 || cnt <= 128) split_node(std::integral_constant<int, 4>{});
+        else split_node(std::integral_constant<int, 8>{});
       }
       // ---- block mode: nodes of more than kSubBig points, the whole block on one node at a time
       for (int bi = 0; bi < nbig; ++bi) {
