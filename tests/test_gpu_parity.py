@@ -114,7 +114,7 @@ def test_golden_veb_layout(gk, oracle):  # SPEC.md:476 / Fig. vebconstruct, thro
 
 
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
-@pytest.mark.parametrize("k", [1, 3, 10, 16, 32, 33, 100, 256])
+@pytest.mark.parametrize("k", [1, 3, 10, 11, 12, 16, 32, 33, 100, 256])
 def test_dims_and_k(gk, oracle, d, k):
     rng = np.random.default_rng(100 * d + k)
     P = rng.random((6000, d))
