@@ -1103,7 +1103,7 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
       // reads, and copy each block of result rows out of the slot PCIe wrote, while the GPU works on the
       // other slots and chunks.  Buffers that are already pinned are copied directly.
       h->ensure_stage();
-      while (h->pev.size() < 2 * nck + 2) {
+      while (h->pev.size() < 3 * nck + 2) {
         cudaEvent_t e;
         GK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         h->pev.push_back(e);
@@ -1111,12 +1111,16 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
       const int nth = std::max(1, std::min(16, host_threads()));
       const bool pq = is_pinned(q), pi = is_pinned(ids), pd = is_pinned(d2);
       cudaEvent_t ev_alloc = h->pev[0], ev_done = h->pev[1];
+      cudaEvent_t* ev_ord = h->pev.data() + 2 + 2 * nck;  // chunk c K2-ordered (on the side stream, as above)
+      cudaStream_t ost = h->bst[0];
       double* dq = dalloc<double>(nq * h->d, h->st);
       std::uint32_t* di = dalloc<std::uint32_t>(nq * k, h->st);
       double* dd = dalloc<double>(nq * k, h->st);
+      std::uint32_t* dperm = dalloc<std::uint32_t>(nq, h->st);
       GK_CUDA(cudaEventRecord(ev_alloc, h->st));
       GK_CUDA(cudaStreamWaitEvent(h->pst[0], ev_alloc, 0));
       GK_CUDA(cudaStreamWaitEvent(h->pst[1], ev_alloc, 0));
+      GK_CUDA(cudaStreamWaitEvent(ost, ev_alloc, 0));
       int slot = 0;
       bool used[gk_bdl::kStageSlots] = {};
       // ring slot for the next transfer: wait until its previous transfer (and copy-out) finished
@@ -1173,8 +1177,11 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
         const std::uint64_t off = bounds[c], m = bounds[c + 1] - off;
         h2d(dq + off * h->d, q + off * h->d, m * h->d * sizeof(double), pq);
         GK_CUDA(cudaEventRecord(h->pev[2 + 2 * c], h->pst[0]));
-        GK_CUDA(cudaStreamWaitEvent(h->st, h->pev[2 + 2 * c], 0));
-        knn_launch(h->d, k, ts, dq + off * h->d, m, di + off * k, dd + off * k, nullptr, h->st, nullptr, nullptr);
+        GK_CUDA(cudaStreamWaitEvent(ost, h->pev[2 + 2 * c], 0));
+        range_order(h->d, dq + off * h->d, m, dperm + off, ost);
+        GK_CUDA(cudaEventRecord(ev_ord[c], ost));
+        GK_CUDA(cudaStreamWaitEvent(h->st, ev_ord[c], 0));
+        knn_traverse(h->d, k, ts, dq + off * h->d, dperm + off, m, di + off * k, dd + off * k, h->st);
         GK_CUDA(cudaEventRecord(h->pev[3 + 2 * c], h->st));
       }
       // rows out, chunk by chunk as they become final
@@ -1190,6 +1197,7 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
       dfree(dq, h->st);
       dfree(di, h->st);
       dfree(dd, h->st);
+      dfree(dperm, h->st);
       GK_CUDA(cudaStreamSynchronize(h->st));
       return;
     }
