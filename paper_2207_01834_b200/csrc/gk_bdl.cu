@@ -1274,12 +1274,14 @@ static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint
           std::uint32_t* ovf = tmp.take<std::uint32_t>(nq);
           const std::uint64_t no =
               range_slots_compact(nq, kRangeSlots, perm, cnt, offs_dev, ti, td, ids_dev, d2_dev, ovf, h->st);
-          if (no)  // the overflowing queries again (in K2 order), rows straight to their offsets
+          if (no) {  // the overflowing queries again (in K2 order), rows straight to their offsets, then sorted
             range_launch(h->d, ts, q_dev, no, r2, r2q_dev, ovf, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
+            range_sort_ovf(ids_dev, d2_dev, total, offs_dev, ovf, no, h->st);
+          }
         } else {
           range_launch(h->d, ts, q_dev, nq, r2, r2q_dev, perm, nullptr, offs_dev, ids_dev, d2_dev, 1, 0, h->st);
+          range_sort(ids_dev, d2_dev, total, offs_dev, nq, h->st);
         }
-        range_sort(ids_dev, d2_dev, total, offs_dev, nq, h->st);
       }
     }
   }

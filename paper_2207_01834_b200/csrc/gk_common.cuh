@@ -235,6 +235,8 @@ std::uint64_t range_slots_compact(std::uint64_t nq, unsigned capq, const std::ui
                                   const double* td, std::uint32_t* ids, double* d2, std::uint32_t* ovf, cudaStream_t st);
 void range_sort(std::uint32_t* ids, double* d2, std::uint64_t total, const unsigned long long* offs, std::uint64_t nq,
                 cudaStream_t st);
+void range_sort_ovf(std::uint32_t* ids, double* d2, std::uint64_t total, const unsigned long long* offs,
+                    const std::uint32_t* ovf, std::uint64_t no, cudaStream_t st);
 // orthogonal (box) range search: ids of live points in [lo, hi] per query, ascending
 void range_box_order(int d, const double* lo, const double* hi, std::uint64_t nq, std::uint32_t* perm, cudaStream_t st);
 void range_box_launch(int d, const TreeSet& trees, const double* lo, const double* hi, std::uint64_t nq,
