@@ -1221,7 +1221,7 @@ int gk_bdl_knn(gk_bdl* h, const double* q, uint64_t nq, int k, uint32_t* ids, do
 // after the offset scan the slots are compacted into the CSR rows and only the queries with
 // more rows than slots are traversed again (their rows straight to their offsets).  Counts
 // only (or a slot buffer that would exceed kRangeSlotBytes): a count traversal.
-constexpr unsigned kRangeSlots = 16;
+constexpr unsigned kRangeSlots = 32;
 constexpr std::uint64_t kRangeSlotBytes = 4ULL << 30;
 static std::uint64_t range_device_impl(gk_bdl* h, const double* q_dev, std::uint64_t nq, double r2,
                                        unsigned long long* counts_dev, unsigned long long* offs_dev, std::uint32_t* ids_dev,

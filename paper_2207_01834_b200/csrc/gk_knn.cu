@@ -935,12 +935,16 @@ void range_d(const TreeSet& ts, const double* Q, std::uint64_t nq, double r2, co
 
 // rows of the bounded-slot pass into their CSR place; flags (in K2 order) the queries with more
 // rows than slots, so that the list of those keeps the order's packet coherence
-constexpr unsigned kRangeSortCap = 16;  // the slot count per query this kernel is written for (kRangeSlots)
-// Slot rows -> CSR rows, each query's rows in (d2, id) order.  A half-warp per query: lane j reads slot j (one
-// coalesced 128-byte + 64-byte read per query instead of 32 lines per load with a thread per query), a 16-lane
-// bitonic network sorts the (d2, id) pairs by shuffles (empty slots = (+inf, ~0) sink to the end), lane j < m
-// writes row j.  (The two CUB segmented sorts over all rows that used to order them took 0.8 ms of a 5.8 ms C2
-// range search; a thread per query with an insertion sort took 0.65 ms for the compaction.)
+constexpr unsigned kRangeSortCap = 32;  // the slot count per query this kernel is written for (kRangeSlots)
+// Slot rows -> CSR rows, each query's rows in (d2, id) order.  A half-warp per query: lane j holds slots j and
+// j + 16 (coalesced reads per query instead of 32 lines per load with a thread per query); a bitonic network
+// sorts the (d2, id) pairs by shuffles -- 16 elements when neither query of the warp has more than 16 rows, else
+// 32 (two per lane; the stride-16 stage is in-lane) -- empty slots = (+inf, ~0) sink to the end; lane j writes
+// rows j and j + 16.  (The two CUB segmented sorts over all rows that used to order them took 0.8 ms of a 5.8 ms
+// C2 range search; a thread per query with an insertion sort took 0.65 ms for the compaction.)
+__device__ __forceinline__ bool pair_less(double a, std::uint32_t ai, double b, std::uint32_t bi) {
+  return a < b || (a == b && ai < bi);
+}
 __global__ void k_slots_compact(std::uint64_t nq, unsigned capq, const std::uint32_t* __restrict__ perm,
                                 const unsigned long long* __restrict__ counts, const unsigned long long* __restrict__ offs,
                                 const std::uint32_t* __restrict__ ti, const double* __restrict__ td,
@@ -958,29 +962,57 @@ __global__ void k_slots_compact(std::uint64_t nq, unsigned capq, const std::uint
   }
   const bool over = c > capq;  // rows come from the second traversal (and its segmented sort)
   const unsigned m = (valid && !over) ? static_cast<unsigned>(c) : 0u;
-  double x = __longlong_as_double(0x7ff0000000000000LL);
-  std::uint32_t xi = 0xffffffffu;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  double x0 = kInf, x1 = kInf;
+  std::uint32_t i0 = 0xffffffffu, i1 = 0xffffffffu;
   if (j < m) {
-    x = td[static_cast<std::uint64_t>(q) * capq + j];
-    xi = ti[static_cast<std::uint64_t>(q) * capq + j];
+    x0 = td[static_cast<std::uint64_t>(q) * capq + j];
+    i0 = ti[static_cast<std::uint64_t>(q) * capq + j];
   }
-  // bitonic sort over the 16 lanes of the half-warp, ascending (d2, id)
+  if (j + 16 < m) {
+    x1 = td[static_cast<std::uint64_t>(q) * capq + j + 16];
+    i1 = ti[static_cast<std::uint64_t>(q) * capq + j + 16];
+  }
+  // compare-exchange of element (x, xi) at position pos with its partner pos ^ s2 in another lane
+  auto cx_shfl = [&](double& x, std::uint32_t& xi, unsigned pos, unsigned k2, unsigned s2) {
+    const double y = __shfl_xor_sync(0xffffffffu, x, s2);
+    const std::uint32_t yi = __shfl_xor_sync(0xffffffffu, xi, s2);
+    const bool up = (pos & k2) == 0, lower = (pos & s2) == 0;
+    const bool less = pair_less(x, xi, y, yi);
+    const bool keep = (lower == up) ? less : !less;
+    if (!keep && !(x == y && xi == yi)) { x = y; xi = yi; }
+  };
+  if (__any_sync(0xffffffffu, m > 16)) {
+    // 32 elements: position p = j (x0) or j + 16 (x1)
 #pragma unroll
-  for (unsigned k2 = 2; k2 <= 16; k2 <<= 1) {
+    for (unsigned k2 = 2; k2 <= 32; k2 <<= 1) {
 #pragma unroll
-    for (unsigned s2 = k2 >> 1; s2 > 0; s2 >>= 1) {
-      const double y = __shfl_xor_sync(0xffffffffu, x, s2);
-      const std::uint32_t yi = __shfl_xor_sync(0xffffffffu, xi, s2);
-      const bool up = (j & k2) == 0;        // this block of k2 lanes sorts ascending
-      const bool lower = (j & s2) == 0;     // this lane keeps the smaller of the pair when ascending
-      const bool less = x < y || (x == y && xi < yi);
-      const bool keep = (lower == up) ? less : !less;  // keep own value?
-      if (!keep && !(x == y && xi == yi)) { x = y; xi = yi; }
+      for (unsigned s2 = k2 >> 1; s2 > 0; s2 >>= 1) {
+        if (s2 == 16) {  // partners are the lane's own two elements (positions j and j + 16; k2 = 32: ascending)
+          if (pair_less(x1, i1, x0, i0)) {
+            const double t = x0; x0 = x1; x1 = t;
+            const std::uint32_t u = i0; i0 = i1; i1 = u;
+          }
+        } else {
+          cx_shfl(x0, i0, j, k2, s2);
+          cx_shfl(x1, i1, j + 16, k2, s2);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (unsigned k2 = 2; k2 <= 16; k2 <<= 1) {
+#pragma unroll
+      for (unsigned s2 = k2 >> 1; s2 > 0; s2 >>= 1) cx_shfl(x0, i0, j, k2, s2);
     }
   }
   if (j < m) {
-    ids[o + j] = xi;
-    d2[o + j] = x;
+    ids[o + j] = i0;
+    d2[o + j] = x0;
+  }
+  if (j + 16 < m) {
+    ids[o + j + 16] = i1;
+    d2[o + j + 16] = x1;
   }
   if (valid && j == 0) flag[i] = over ? 1 : 0;
 }
@@ -1215,7 +1247,7 @@ void range_launch(int d, const TreeSet& trees, const double* q_dev, std::uint64_
 std::uint64_t range_slots_compact(std::uint64_t nq, unsigned capq, const std::uint32_t* perm,
                                   const unsigned long long* counts, const unsigned long long* offs, const std::uint32_t* ti,
                                   const double* td, std::uint32_t* ids, double* d2, std::uint32_t* ovf, cudaStream_t st) {
-  if (capq != kRangeSortCap) throw Error(GK_ERR_LOGIC, "k_slots_compact is written for 16 slots per query");
+  if (capq != kRangeSortCap) throw Error(GK_ERR_LOGIC, "k_slots_compact is written for 32 slots per query");
   std::uint8_t* flag = nullptr;
   unsigned long long* nsel = nullptr;
   GK_CUDA(cudaMallocAsync(&flag, nq, st));
