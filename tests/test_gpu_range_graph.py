@@ -40,9 +40,10 @@ def test_range_parity(gk, oracle, d):
     E = P[rng.choice(len(P), 2_000, replace=False)]
     assert g.erase(E) == o.erase(E)
     Q = np.concatenate([rng.random((3_000, d)), P[:500]])
-    # r2 giving ~ 0, ~ 1, ~ 20 points per query, then exact duplicates only
+    # r2 giving ~ 0.5, ~ 20 and ~ 40 points per query (below / around / above the 32 slots per query), then exact
+    # duplicates only
     vol = {2: np.pi, 3: 4.18879, 5: 5.26379, 7: 4.72477, 8: 4.05871}[d]
-    for mean in (0.5, 20.0):
+    for mean in (0.5, 20.0, 40.0):  # 40: most queries above the 32 slots (second traversal + segmented sort)
         r2 = float((mean / len(P) / vol) ** (2.0 / d))
         _same(g.range(Q, r2), o.range(Q, r2), f"d={d} r2={r2}")
         assert np.array_equal(g.range_count(Q, r2), np.diff(o.range(Q, r2)[0]))
